@@ -1,0 +1,205 @@
+// C ABI layer: argument validation (host), sequence-split planning, dispatch.
+// Error behaviour mirrors the reference: shape/plan problems are
+// LBS_ERR_INVALID, which the Python host maps to lbscan's ShapeError
+// (core.py:24-25, engine.py:56-57,221-243); the hot path does not scan for
+// NaN (the reference engine does not either, engine.py:221-236).
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "lbs_common.cuh"
+#include "lbs_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return LBS_OK;
+  return fail(LBS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool io_dtype_ok(int d) { return d == LBS_F32 || d == LBS_BF16 || d == LBS_F16; }
+
+constexpr int kNumSMs = 148;
+
+// states padded per thread (kernels instantiate NS in {4, 8, 16})
+int padded_states(int64_t N) { return N <= 4 ? 4 : (N <= 8 ? 8 : 16); }
+
+// Sequence-split plan: cut L into S segments (multiples of the window) only
+// when B*E alone cannot fill the machine; each extra segment costs one extra
+// aggregate pass over its steps, so S stays as small as possible.
+void plan_segments(const lbs_scan_fwd_args* a, int* n_seg, int* seg_len) {
+  const int64_t L = a->seqlen, m = a->window;
+  const int64_t ctas = ((a->dim + lbs::kFwdThreads - 1) / lbs::kFwdThreads) * a->batch;
+  const int64_t warps = ((a->dim + 31) / 32) * a->batch;
+  int64_t S = 1;
+  if (a->seg_hint > 0) {
+    S = a->seg_hint;
+  } else if (warps < 4 * kNumSMs && L >= 1024) {
+    // aim for ~8 resident warps per SM, segments no shorter than 256 steps
+    S = (8 * kNumSMs + warps - 1) / warps;
+    (void)ctas;
+    const int64_t max_s = L / 256;
+    if (S > max_s) S = max_s;
+    if (S > 256) S = 256;
+    if (S < 1) S = 1;
+  }
+  int64_t len = (L + S - 1) / S;
+  len = ((len + m - 1) / m) * m;  // segment boundaries on tile boundaries
+  S = (L + len - 1) / len;
+  *n_seg = (int)S;
+  *seg_len = (int)len;
+}
+
+int validate_fwd(const lbs_scan_fwd_args* a) {
+  if (!a) return fail(LBS_ERR_INVALID, "null args");
+  if (a->batch < 1 || a->seqlen < 1 || a->dim < 1 || a->dstate < 1)
+    return fail(LBS_ERR_INVALID, "all dimensions must be >= 1 (B=%lld L=%lld E=%lld N=%lld)",
+                (long long)a->batch, (long long)a->seqlen, (long long)a->dim, (long long)a->dstate);
+  if (a->window < 1) return fail(LBS_ERR_INVALID, "tile length must be >= 1, got %lld", (long long)a->window);
+  if (a->batch > 65535) return fail(LBS_ERR_UNSUPPORTED, "batch > 65535");
+  if (a->seqlen > (int64_t)1 << 30 || a->dim > (int64_t)1 << 24)
+    return fail(LBS_ERR_UNSUPPORTED, "sequence or channel count too large");
+  if (!io_dtype_ok(a->io_dtype)) return fail(LBS_ERR_INVALID, "bad io dtype %d", a->io_dtype);
+  if (!io_dtype_ok(a->bc_dtype)) return fail(LBS_ERR_INVALID, "bad B/C dtype %d", a->bc_dtype);
+  if (!a->u || !a->delta || !a->A || !a->B || !a->C || !a->out)
+    return fail(LBS_ERR_INVALID, "u, delta, A, B, C and out must be non-null");
+  if (a->dstate > 16)
+    return fail(LBS_ERR_UNSUPPORTED, "dstate %lld > 16 is not supported by the fused kernel",
+                (long long)a->dstate);
+  if (a->window > 16 && a->window < a->seqlen)
+    return fail(LBS_ERR_UNSUPPORTED, "window %lld > 16 (with window < L) is not supported yet",
+                (long long)a->window);
+  if (a->checkpoints && (a->ckpt_len < 1 || a->ckpt_len % a->window))
+    return fail(LBS_ERR_INVALID, "ckpt_len must be a positive multiple of the window");
+  return LBS_OK;
+}
+
+lbs::View3D view(const void* p, const int64_t* s) { return lbs::View3D{p, s[0], s[1], s[2]}; }
+
+void fill_fwd_params(const lbs_scan_fwd_args* a, lbs::FwdParams* p) {
+  p->Bt = (int)a->batch;
+  p->L = (int)a->seqlen;
+  p->E = (int)a->dim;
+  p->N = (int)a->dstate;
+  // a window longer than the sequence is one (ragged) tile (test_oracle.py:247-252)
+  p->m = (int)(a->window > a->seqlen ? a->seqlen : a->window);
+  if (p->m > 16) p->m = p->L;  // unreachable after validation unless m >= L
+  p->flags = a->flags;
+  p->u = view(a->u, a->u_stride);
+  p->delta = view(a->delta, a->delta_stride);
+  p->z = view(a->z, a->z_stride);
+  p->Bm = view(a->B, a->B_stride);
+  p->Cm = view(a->C, a->C_stride);
+  p->out = a->out;
+  p->so0 = a->out_stride[0];
+  p->so1 = a->out_stride[1];
+  p->so2 = a->out_stride[2];
+  p->A = a->A;
+  p->D = a->D;
+  p->bias = a->delta_bias;
+  p->last_state = a->last_state;
+  p->ckpt = a->checkpoints;
+  p->ckpt_len = (int)a->ckpt_len;
+  p->n_ckpt = a->checkpoints ? (int)((a->seqlen + a->ckpt_len - 1) / a->ckpt_len) : 0;
+}
+
+}  // namespace
+
+namespace lbs {
+int fwd_padded_states(int N) { return padded_states(N); }
+}  // namespace lbs
+
+extern "C" {
+
+int lbs_set_error(int code, const char* msg) { return fail(code, "%s", msg); }
+
+int lbs_abi_version(void) { return LBS_ABI_VERSION; }
+
+const char* lbs_last_error(void) { return g_err.c_str(); }
+
+int64_t lbs_select_tile_len(int64_t L) {
+  // engine.py:54-62
+  if (L < 1) return -1;
+  if (L > 256) return 16;
+  if (L > 128) return 8;
+  return 4;
+}
+
+size_t lbs_scan_fwd_workspace_bytes(const lbs_scan_fwd_args* a) {
+  if (validate_fwd(a) != LBS_OK) return 0;
+  lbs_scan_fwd_args b = *a;
+  if (b.window > b.seqlen) b.window = b.seqlen;
+  int S, len;
+  plan_segments(&b, &S, &len);
+  if (S <= 1) return 0;
+  return (size_t)a->batch * S * a->dim * 2 * padded_states(a->dstate) * sizeof(float);
+}
+
+int lbs_scan_fwd(const lbs_scan_fwd_args* a, void* ws, size_t ws_bytes, void* stream) {
+  int rc = validate_fwd(a);
+  if (rc != LBS_OK) return rc;
+  lbs::FwdParams p{};
+  fill_fwd_params(a, &p);
+  lbs_scan_fwd_args b = *a;
+  b.window = p.m;
+  plan_segments(&b, &p.n_seg, &p.seg_len);
+  if (p.n_seg > 1) {
+    const size_t need = (size_t)a->batch * p.n_seg * a->dim * 2 * padded_states(a->dstate) * sizeof(float);
+    if (!ws || ws_bytes < need)
+      return fail(LBS_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    p.seg_agg = static_cast<float*>(ws);
+  }
+  if (p.ckpt) return fail(LBS_ERR_UNSUPPORTED, "forward checkpoints not implemented yet");
+  return cuda_status(lbs::launch_fwd(p, a->io_dtype, a->bc_dtype, (cudaStream_t)stream), "lbs_scan_fwd");
+}
+
+int lbs_prediscretized_fwd(const lbs_prediscretized_args* a, void* stream) {
+  if (!a) return fail(LBS_ERR_INVALID, "null args");
+  if (a->batch < 1 || a->seqlen < 1 || a->dim < 1 || a->dstate < 1)
+    return fail(LBS_ERR_INVALID, "all dimensions must be >= 1");
+  if (a->window < 1) return fail(LBS_ERR_INVALID, "tile length must be >= 1, got %lld", (long long)a->window);
+  if (a->dstate > 64) return fail(LBS_ERR_UNSUPPORTED, "dstate > 64");
+  if (a->dtype != LBS_F32 && a->dtype != LBS_F64) return fail(LBS_ERR_INVALID, "dtype must be f32 or f64");
+  if (!a->abar || !a->bx || !a->c || !a->dx || !a->y || !a->h_final)
+    return fail(LBS_ERR_INVALID, "null tensor");
+  if (a->batch > 65535) return fail(LBS_ERR_UNSUPPORTED, "batch > 65535");
+  lbs::PreParams p{};
+  p.Bt = (int)a->batch;
+  p.L = (int)a->seqlen;
+  p.E = (int)a->dim;
+  p.N = (int)a->dstate;
+  p.m = (int)(a->window > a->seqlen ? a->seqlen : a->window);
+  p.flags = a->flags;
+  p.abar = a->abar;
+  p.bx = a->bx;
+  p.c = a->c;
+  p.dx = a->dx;
+  p.y = a->y;
+  p.h_final = a->h_final;
+  return cuda_status(lbs::launch_prediscretized(p, a->dtype == LBS_F64, (cudaStream_t)stream),
+                     "lbs_prediscretized_fwd");
+}
+
+size_t lbs_scan_bwd_workspace_bytes(const lbs_scan_bwd_args* a) {
+  (void)a;
+  return 0;
+}
+
+int lbs_scan_bwd(const lbs_scan_bwd_args* a, void* ws, size_t ws_bytes, void* stream) {
+  (void)a; (void)ws; (void)ws_bytes; (void)stream;
+  return fail(LBS_ERR_UNSUPPORTED, "lbs_scan_bwd not implemented yet");
+}
+
+}  // extern "C"

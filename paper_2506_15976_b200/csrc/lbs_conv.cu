@@ -1,0 +1,257 @@
+// Depthwise causal conv1d (+ fused SiLU), channel-last, with flip-on-load.
+//
+// Forward replaces nn.causal_conv1d + nn.silu (nn.py:87-99,25-26):
+//   xc[l] = sum_{q<K} w[e,q] x[l-q] (+ bias),  out = silu(xc)
+// Backward replaces nn.causal_conv1d_grad + silu_grad (nn.py:102-114,29-31),
+// recomputing xc instead of storing it:
+//   g = dout * silu'(xc);  dx[l] = sum_q w[e,q] g[l+q];  dw[e,q] = sum_{b,l} g[l] x[l-q]
+// "l" is the logical (scanned) index; with LBS_FLAG_REVERSE logical l reads
+// physical L-1-l, so LBVim's reverse-direction layers need no flip copies
+// (block.py:180-181, model.py:216-218).
+//
+// HBM-bound elementwise kernel: one thread per (b, e, chunk of kConvChunk
+// steps) keeps the K-1 step history in registers; a warp covers 32
+// consecutive channels, so every step is one contiguous row segment.
+#include <string>
+
+#include "lbs_common.cuh"
+#include "lbs_internal.h"
+
+namespace lbs {
+
+constexpr int kConvThreads = 128;
+constexpr int kConvChunk = 32;
+constexpr int kMaxWidth = 8;
+
+struct ConvParams {
+  int Bt, L, E, K;
+  uint32_t flags;
+  View3D x, dout;
+  void* out;
+  long long so0, so1, so2;
+  void* dx;
+  long long sd0, sd1, sd2;
+  const float* w;
+  const float* bias;
+  float* part;  // (n_part, E, K+1) dweight/dbias partials
+  int n_chunks;
+};
+
+template <typename T, int KW>
+__global__ void __launch_bounds__(kConvThreads) conv_fwd_kernel(ConvParams p) {
+  const int e = blockIdx.x * kConvThreads + threadIdx.x;
+  if (e >= p.E) return;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  const int L = p.L;
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  float w[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) w[q] = q < p.K ? p.w[(long long)e * p.K + q] : 0.f;
+  const float bias = p.bias ? p.bias[e] : 0.f;
+  const T* xp = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + (long long)e * p.x.s2;
+  T* op = static_cast<T*>(p.out) + (long long)b * p.so0 + (long long)e * p.so2;
+  const int l0 = chunk * kConvChunk;
+  const int l1 = min(L, l0 + kConvChunk);
+  auto phys = [&](int l) -> long long { return rev ? (L - 1 - l) : l; };
+  float hist[KW];  // hist[q] = x[l - q]
+  hist[0] = 0.f;
+#pragma unroll
+  for (int q = 1; q < KW; ++q) {
+    const int l = l0 - q;
+    hist[q] = (q < p.K && l >= 0) ? ld<T>(xp + phys(l) * p.x.s1) : 0.f;
+  }
+  for (int l = l0; l < l1; ++l) {
+    hist[0] = ld<T>(xp + phys(l) * p.x.s1);
+    float acc = bias;
+#pragma unroll
+    for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], hist[q], acc);
+    st<T>(op + phys(l) * p.so1, act ? silu_f(acc) : acc);
+#pragma unroll
+    for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
+  }
+}
+
+template <typename T, int KW>
+__global__ void __launch_bounds__(kConvThreads) conv_bwd_kernel(ConvParams p) {
+  const int e = blockIdx.x * kConvThreads + threadIdx.x;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  if (e >= p.E) return;
+  const int L = p.L, K = p.K;
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  float w[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) w[q] = q < K ? p.w[(long long)e * K + q] : 0.f;
+  const float bias = p.bias ? p.bias[e] : 0.f;
+  const T* xp = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + (long long)e * p.x.s2;
+  const T* gp = static_cast<const T*>(p.dout.p) + (long long)b * p.dout.s0 + (long long)e * p.dout.s2;
+  T* dxp = static_cast<T*>(p.dx) + (long long)b * p.sd0 + (long long)e * p.sd2;
+  auto phys = [&](int l) -> long long { return rev ? (L - 1 - l) : l; };
+  auto X = [&](int l) -> float { return (l >= 0 && l < L) ? ld<T>(xp + phys(l) * p.x.s1) : 0.f; };
+  // g[l] = dout[l] * silu'(xc[l]); xc recomputed from x
+  auto G = [&](int l) -> float {
+    if (l < 0 || l >= L) return 0.f;
+    float gv = ld<T>(gp + phys(l) * p.dout.s1);
+    if (act) {
+      float xc = bias;
+#pragma unroll
+      for (int q = 0; q < KW; ++q)
+        if (q < K) xc = fmaf(w[q], X(l - q), xc);
+      const float s = sigmoid_f(xc);
+      gv *= s * (1.f + xc * (1.f - s));
+    }
+    return gv;
+  };
+  const int l0 = chunk * kConvChunk;
+  const int l1 = min(L, l0 + kConvChunk);
+  float dw[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) dw[q] = 0.f;
+  float db = 0.f;
+  // sliding window of future g: fut[q] = g[l + q]
+  float fut[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) fut[q] = (q < K) ? G(l0 + q) : 0.f;
+  for (int l = l0; l < l1; ++l) {
+    float acc = 0.f;
+#pragma unroll
+    for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], fut[q], acc);
+    st<T>(dxp + phys(l) * p.sd1, acc);
+    const float g0 = fut[0];
+    db += g0;
+#pragma unroll
+    for (int q = 0; q < KW; ++q)
+      if (q < K) dw[q] = fmaf(g0, X(l - q), dw[q]);
+#pragma unroll
+    for (int q = 0; q < KW - 1; ++q) fut[q] = fut[q + 1];
+    fut[KW - 1] = 0.f;
+    if (K >= 1) {
+      // fill slot K-1 with g[l + K]
+      float nxt = G(l + K);
+#pragma unroll
+      for (int q = 0; q < KW; ++q)
+        if (q == K - 1) fut[q] = nxt;
+    }
+  }
+  float* part = p.part + (((long long)b * p.n_chunks + chunk) * p.E + e) * (K + 1);
+  for (int q = 0; q < K; ++q) part[q] = dw[q];
+  part[K] = db;
+}
+
+// deterministic reduction of the (B * n_chunks) partials -> dweight, dbias (+=)
+__global__ void conv_reduce_kernel(const float* part, int n_part, int E, int K, float* dw, float* db) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= E * (K + 1)) return;
+  double s = 0.0;
+  for (int i = 0; i < n_part; ++i) s += part[(long long)i * E * (K + 1) + idx];
+  const int e = idx / (K + 1), q = idx - e * (K + 1);
+  if (q < K) dw[(long long)e * K + q] += (float)s;
+  else if (db) db[e] += (float)s;
+}
+
+template <typename T>
+static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
+  dim3 grid((p.E + kConvThreads - 1) / kConvThreads, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
+  if (p.K <= 4) conv_fwd_kernel<T, 4><<<grid, kConvThreads, 0, st>>>(p);
+  else conv_fwd_kernel<T, kMaxWidth><<<grid, kConvThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t conv_bwd_t(const ConvParams& p, float* dw, float* db, cudaStream_t st) {
+  dim3 grid((p.E + kConvThreads - 1) / kConvThreads, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
+  if (p.K <= 4) conv_bwd_kernel<T, 4><<<grid, kConvThreads, 0, st>>>(p);
+  else conv_bwd_kernel<T, kMaxWidth><<<grid, kConvThreads, 0, st>>>(p);
+  const int n = p.E * (p.K + 1);
+  conv_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(p.part, p.Bt * p.n_chunks, p.E, p.K, dw, db);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv_fwd(const ConvParams& p, int dtype, cudaStream_t st) {
+  if (dtype == LBS_F32) return conv_fwd_t<float>(p, st);
+  if (dtype == LBS_BF16) return conv_fwd_t<__nv_bfloat16>(p, st);
+  return conv_fwd_t<__half>(p, st);
+}
+
+cudaError_t launch_conv_bwd(const ConvParams& p, int dtype, float* dw, float* db, cudaStream_t st) {
+  if (dtype == LBS_F32) return conv_bwd_t<float>(p, dw, db, st);
+  if (dtype == LBS_BF16) return conv_bwd_t<__nv_bfloat16>(p, dw, db, st);
+  return conv_bwd_t<__half>(p, dw, db, st);
+}
+
+}  // namespace lbs
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+namespace {
+int conv_validate(const lbs_conv_args* a, bool bwd, std::string* err) {
+  if (!a) { *err = "null args"; return LBS_ERR_INVALID; }
+  if (a->batch < 1 || a->seqlen < 1 || a->dim < 1 || a->width < 1) {
+    *err = "all dimensions must be >= 1";
+    return LBS_ERR_INVALID;
+  }
+  if (a->width > lbs::kMaxWidth) { *err = "conv width > 8 unsupported"; return LBS_ERR_UNSUPPORTED; }
+  if (a->io_dtype != LBS_F32 && a->io_dtype != LBS_BF16 && a->io_dtype != LBS_F16) {
+    *err = "bad dtype";
+    return LBS_ERR_INVALID;
+  }
+  if (a->batch > 65535) { *err = "batch > 65535"; return LBS_ERR_UNSUPPORTED; }
+  if (!a->x || !a->weight) { *err = "x and weight must be non-null"; return LBS_ERR_INVALID; }
+  if (!bwd && !a->out) { *err = "out must be non-null"; return LBS_ERR_INVALID; }
+  if (bwd && (!a->dout || !a->dx || !a->dweight)) { *err = "dout, dx, dweight must be non-null"; return LBS_ERR_INVALID; }
+  return LBS_OK;
+}
+
+lbs::ConvParams conv_params(const lbs_conv_args* a) {
+  lbs::ConvParams p{};
+  p.Bt = (int)a->batch;
+  p.L = (int)a->seqlen;
+  p.E = (int)a->dim;
+  p.K = (int)a->width;
+  p.flags = a->flags;
+  p.x = lbs::View3D{a->x, a->x_stride[0], a->x_stride[1], a->x_stride[2]};
+  p.dout = lbs::View3D{a->dout, a->dout_stride[0], a->dout_stride[1], a->dout_stride[2]};
+  p.out = a->out;
+  p.so0 = a->out_stride[0]; p.so1 = a->out_stride[1]; p.so2 = a->out_stride[2];
+  p.dx = a->dx;
+  p.sd0 = a->dx_stride[0]; p.sd1 = a->dx_stride[1]; p.sd2 = a->dx_stride[2];
+  p.w = a->weight;
+  p.bias = a->bias;
+  p.n_chunks = (int)((a->seqlen + lbs::kConvChunk - 1) / lbs::kConvChunk);
+  return p;
+}
+}  // namespace
+
+extern "C" int lbs_set_error(int code, const char* msg);
+
+extern "C" size_t lbs_causal_conv1d_bwd_workspace_bytes(const lbs_conv_args* a) {
+  std::string err;
+  if (conv_validate(a, true, &err) != LBS_OK) return 0;
+  const size_t nch = (a->seqlen + lbs::kConvChunk - 1) / lbs::kConvChunk;
+  return (size_t)a->batch * nch * a->dim * (a->width + 1) * sizeof(float);
+}
+
+extern "C" int lbs_causal_conv1d_fwd(const lbs_conv_args* a, void* stream) {
+  std::string err;
+  int rc = conv_validate(a, false, &err);
+  if (rc != LBS_OK) return lbs_set_error(rc, err.c_str());
+  lbs::ConvParams p = conv_params(a);
+  cudaError_t e = lbs::launch_conv_fwd(p, a->io_dtype, (cudaStream_t)stream);
+  if (e != cudaSuccess) return lbs_set_error(LBS_ERR_CUDA, cudaGetErrorString(e));
+  return LBS_OK;
+}
+
+extern "C" int lbs_causal_conv1d_bwd(const lbs_conv_args* a, void* ws, size_t ws_bytes, void* stream) {
+  std::string err;
+  int rc = conv_validate(a, true, &err);
+  if (rc != LBS_OK) return lbs_set_error(rc, err.c_str());
+  const size_t need = lbs_causal_conv1d_bwd_workspace_bytes(a);
+  if (!ws || ws_bytes < need) return lbs_set_error(LBS_ERR_INVALID, "conv bwd workspace too small");
+  lbs::ConvParams p = conv_params(a);
+  p.part = static_cast<float*>(ws);
+  cudaError_t e = lbs::launch_conv_bwd(p, a->io_dtype, a->dweight, a->dbias, (cudaStream_t)stream);
+  if (e != cudaSuccess) return lbs_set_error(LBS_ERR_CUDA, cudaGetErrorString(e));
+  return LBS_OK;
+}

@@ -1,0 +1,50 @@
+// Internal (host+device) parameter blocks shared by the kernels and the C ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lbs {
+
+constexpr int kFwdThreads = 128;  // channels per CTA
+constexpr int kFwdChunk = 64;     // steps of B/C staged in shared memory per chunk
+
+struct View3D {
+  const void* p;
+  long long s0, s1, s2;
+};
+
+struct FwdParams {
+  int Bt, L, E, N, m;
+  uint32_t flags;
+  View3D u, delta, z, Bm, Cm;
+  void* out;
+  long long so0, so1, so2;
+  const float* A;
+  const float* D;
+  const float* bias;
+  float* last_state;
+  // sequence split
+  int n_seg, seg_len;
+  float* seg_agg;  // (Bt, n_seg, E, 2*NS) fp32 workspace
+  // training checkpoints (state entering each ckpt chunk)
+  float* ckpt;
+  int ckpt_len, n_ckpt;
+};
+
+cudaError_t launch_fwd(const FwdParams& p, int io_dtype, int bc_dtype, cudaStream_t st);
+int fwd_padded_states(int N);  // NS used by the kernels for a given N
+
+struct PreParams {
+  int Bt, L, E, N, m;
+  uint32_t flags;
+  const void* abar;
+  const void* bx;
+  const void* c;
+  const void* dx;
+  void* y;
+  void* h_final;
+};
+cudaError_t launch_prediscretized(const PreParams& p, bool f64, cudaStream_t st);
+
+}  // namespace lbs

@@ -1,0 +1,183 @@
+"""Host side of the fused LB selective scan (PyTorch tensors -> C ABI).
+
+North-star operator API:
+
+    lbm_selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None,
+                       delta_softplus=True, window=None, reverse=False,
+                       return_last_state=False)
+
+in the reference's channel-last layout (core.py:8-14): ``u``, ``delta``, ``z``
+are (B, L, E); ``B``, ``C`` are (B, L, N); ``A`` is (E, N); ``D`` and
+``delta_bias`` are (E,).  The composition it computes is exactly
+block.py:90-98 + engine.lbm_scan_par + block.py:177-178:
+
+    dl = softplus(delta + delta_bias);  abar = exp(dl (x) A);  bx = (dl*u) (x) B
+    y  = lbm(abar, bx, C, D*u, M);      out = y * silu(z)
+
+``window`` defaults to ``select_tile_len(L)`` (engine.py:54-62); ``reverse``
+scans right-to-left by flip-on-load (no copies).  Any strides are accepted
+(e.g. B and C as column slices of one fused projection output).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import FLAG_LB, FLAG_LINEAR, FLAG_REVERSE, FLAG_SOFTPLUS
+from .errors import ShapeError
+from .tiling import select_tile_len
+
+_DT = {torch.float32: _lib.LBS_F32, torch.bfloat16: _lib.LBS_BF16, torch.float16: _lib.LBS_F16}
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _strides(t):
+    return _lib.I64x3(*t.stride()) if t is not None else _lib.I64x3(0, 0, 0)
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need_cuda(name, t):
+    if t is not None and not t.is_cuda:
+        raise ShapeError(f"{name} must be a CUDA tensor (the product path has no CPU fallback)")
+
+
+def _vec(name, t, E, device):
+    if t is None:
+        return None
+    t = torch.as_tensor(t, device=device)
+    if t.shape != (E,):
+        raise ShapeError(f"{name} has shape {tuple(t.shape)}, expected {(E,)}")
+    return t.to(torch.float32).contiguous()
+
+
+def _prepare(u, delta, A, B, C_, D, z, delta_bias, window):
+    for name, t in (("u", u), ("delta", delta), ("B", B), ("C", C_), ("z", z)):
+        _need_cuda(name, t)
+    if u.dim() != 3:
+        raise ShapeError(f"u must be (B, L, E), got {tuple(u.shape)}")
+    Bt, L, E = u.shape
+    if min(Bt, L, E) < 1:
+        raise ShapeError(f"u has a zero-length dimension: {tuple(u.shape)}")
+    if delta.shape != u.shape:
+        raise ShapeError(f"delta has shape {tuple(delta.shape)}, expected {tuple(u.shape)}")
+    if z is not None and z.shape != u.shape:
+        raise ShapeError(f"z has shape {tuple(z.shape)}, expected {tuple(u.shape)}")
+    A = torch.as_tensor(A, device=u.device)
+    if A.dim() != 2 or A.shape[0] != E:
+        raise ShapeError(f"A must be (E, N) = ({E}, N), got {tuple(A.shape)}")
+    N = A.shape[1]
+    for name, t in (("B", B), ("C", C_)):
+        if t.shape != (Bt, L, N):
+            raise ShapeError(f"{name} has shape {tuple(t.shape)}, expected {(Bt, L, N)}")
+    if u.dtype not in _DT:
+        u = u.to(torch.float32)
+    io = u.dtype
+    delta = delta.to(io)
+    if z is not None:
+        z = z.to(io)
+    bc = B.dtype if B.dtype in _DT else torch.float32
+    if bc != io and not (io == torch.bfloat16 and bc == torch.float32):
+        bc = io
+    B = B.to(bc)
+    C_ = C_.to(bc)
+    M = select_tile_len(L) if window in (None, "auto") else int(window)
+    if M < 1:
+        raise ShapeError(f"tile length must be >= 1, got {M}")
+    A = A.to(torch.float32).contiguous()
+    D = _vec("D", D, E, u.device)
+    delta_bias = _vec("delta_bias", delta_bias, E, u.device)
+    return u, delta, A, B, C_, D, z, delta_bias, M, (Bt, L, E, N)
+
+
+def _fwd_args(u, delta, A, B, C_, D, z, delta_bias, M, dims, flags, out, last_state, seg_hint=0):
+    Bt, L, E, N = dims
+    a = _lib.ScanFwdArgs()
+    a.batch, a.seqlen, a.dim, a.dstate, a.window = Bt, L, E, N, M
+    a.io_dtype = _DT[u.dtype]
+    a.bc_dtype = _DT[B.dtype]
+    a.flags = flags
+    a.seg_hint = seg_hint
+    a.u, a.u_stride = _ptr(u), _strides(u)
+    a.delta, a.delta_stride = _ptr(delta), _strides(delta)
+    a.A = _ptr(A)
+    a.B, a.B_stride = _ptr(B), _strides(B)
+    a.C, a.C_stride = _ptr(C_), _strides(C_)
+    a.D = _ptr(D)
+    a.delta_bias = _ptr(delta_bias)
+    a.z, a.z_stride = _ptr(z), _strides(z)
+    a.out, a.out_stride = _ptr(out), _strides(out)
+    a.last_state = _ptr(last_state)
+    a.checkpoints = None
+    a.ckpt_len = 0
+    return a
+
+
+def _flags(delta_softplus, reverse, lb, mode):
+    if mode not in ("exp", "linear"):
+        raise ShapeError(f"unknown discretize mode {mode!r}")  # block.py:88-89
+    f = 0
+    if delta_softplus:
+        f |= FLAG_SOFTPLUS
+    if reverse:
+        f |= FLAG_REVERSE
+    if lb:
+        f |= FLAG_LB
+    if mode == "linear":
+        f |= FLAG_LINEAR
+    return f
+
+
+def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
+                           delta_softplus=True, window=None, reverse=False,
+                           return_last_state=False, lb=True, discretize_mode="exp",
+                           out=None, seg_hint=0):
+    """Forward launch (no autograd).  Returns ``out`` or ``(out, last_state)``."""
+    u, delta, A, B, C, D, z, delta_bias, M, dims = _prepare(u, delta, A, B, C, D, z, delta_bias, window)
+    Bt, L, E, N = dims
+    if out is None:
+        out = torch.empty((Bt, L, E), dtype=u.dtype, device=u.device)
+    last = torch.empty((Bt, E, N), dtype=torch.float32, device=u.device) if return_last_state else None
+    flags = _flags(delta_softplus, reverse, lb, discretize_mode)
+    args = _fwd_args(u, delta, A, B, C, D, z, delta_bias, M, dims, flags, out, last, seg_hint)
+    L_ = _lib.lib()
+    nws = L_.lbs_scan_fwd_workspace_bytes(ctypes.byref(args))
+    ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=u.device) if nws else None
+    rc = L_.lbs_scan_fwd(ctypes.byref(args), _ptr(ws), nws, _stream())
+    _lib.check(rc, "lbm_selective_scan")
+    return (out, last) if return_last_state else out
+
+
+def lbm_selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None,
+                       delta_softplus=True, window=None, reverse=False,
+                       return_last_state=False, discretize_mode="exp"):
+    """The north-star fused operator (LB scan).  Differentiable when any input
+    requires grad (backward = lbs_scan_bwd)."""
+    needs_grad = torch.is_grad_enabled() and any(
+        t is not None and isinstance(t, torch.Tensor) and t.requires_grad
+        for t in (u, delta, A, B, C, D, z, delta_bias))
+    if needs_grad:
+        from .autograd import LbmSelectiveScanFn
+        out = LbmSelectiveScanFn.apply(u, delta, A, B, C, D, z, delta_bias, delta_softplus,
+                                       window, reverse, True, discretize_mode)
+        if return_last_state:
+            raise NotImplementedError("return_last_state with autograd")
+        return out
+    return lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, window,
+                                  reverse, return_last_state, True, discretize_mode)
+
+
+def selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_softplus=True,
+                   reverse=False, return_last_state=False):
+    """Plain unidirectional selective scan (engine.forward_scan_par semantics,
+    engine.py:294) — the same kernel with the LB pass compiled out."""
+    return lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 1,
+                                  reverse, return_last_state, False)

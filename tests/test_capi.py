@@ -1,0 +1,81 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol the
+header declares, and validates arguments (ShapeError mapping) before any
+device work."""
+
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2506_15976_b200 import _lib
+from paper_2506_15976_b200.errors import ShapeError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "lbscan_b200.h")).read()
+    return sorted(set(re.findall(r"\b(lbs_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    declared = header_symbols()
+    assert len(declared) >= 11
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(declared) == set(_lib.EXPORTS)
+
+
+def test_abi_version_and_tile_rule():
+    L = _lib.lib()
+    assert L.lbs_abi_version() == 1
+    # engine.py:54-62 / test_engine.py:11-19
+    for Ln, M in ((1024, 16), (257, 16), (256, 8), (200, 8), (129, 8), (128, 4), (64, 4), (1, 4)):
+        assert L.lbs_select_tile_len(Ln) == M
+    assert L.lbs_select_tile_len(0) == -1
+
+
+def _args(**kw):
+    a = _lib.ScanFwdArgs()
+    a.batch, a.seqlen, a.dim, a.dstate, a.window = 2, 8, 4, 4, 4
+    a.io_dtype = a.bc_dtype = _lib.LBS_F32
+    a.flags = _lib.FLAG_LB | _lib.FLAG_SOFTPLUS
+    fake = C.c_void_p(0x1000)
+    for f in ("u", "delta", "A", "B", "C", "out"):
+        setattr(a, f, fake)
+    for k, v in kw.items():
+        setattr(a, k, v)
+    return a
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(seqlen=0), "dimensions"),
+    (dict(window=0), "tile length"),
+    (dict(io_dtype=9), "dtype"),
+    (dict(u=None), "non-null"),
+])
+def test_invalid_arguments_raise_shape_error(kw, msg):
+    L = _lib.lib()
+    rc = L.lbs_scan_fwd(C.byref(_args(**kw)), None, 0, None)
+    assert rc == _lib.LBS_ERR_INVALID
+    assert msg in L.lbs_last_error().decode()
+    with pytest.raises(ShapeError):
+        _lib.check(rc, "lbm_selective_scan")
+
+
+def test_prediscretized_rejects_bad_window():
+    L = _lib.lib()
+    a = _lib.PrediscretizedArgs()
+    a.batch, a.seqlen, a.dim, a.dstate, a.window = 1, 4, 2, 2, 0
+    a.dtype = _lib.LBS_F32
+    assert L.lbs_prediscretized_fwd(C.byref(a), None) == _lib.LBS_ERR_INVALID
+
+
+def test_python_api_rejects_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    from paper_2506_15976_b200.scan import lbm_selective_scan
+    x = torch.zeros(1, 4, 2)
+    with pytest.raises(ShapeError):
+        lbm_selective_scan(x, x, torch.zeros(2, 3), torch.zeros(1, 4, 3), torch.zeros(1, 4, 3))

@@ -1,0 +1,248 @@
+"""Parity of the sm_100a forward kernels with the CPU oracle (pinned to the
+reference by tests/test_oracle_golden.py).  Runs on the B200 box: -m gpu."""
+
+import os
+
+import numpy as np
+import pytest
+
+from helpers import TOL_BF16, TOL_F32, op_inputs
+from oracle import lbscan_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2506_15976_b200 import engine  # noqa: E402
+from paper_2506_15976_b200.scan import lbm_selective_scan, lbm_selective_scan_fwd, selective_scan  # noqa: E402
+from paper_2506_15976_b200.tiling import TilePlan  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def dev(x, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+def run_gpu(inp, dtype=torch.float32, **kw):
+    t = {k: (dev(v, dtype) if k in ("u", "delta", "z", "B", "C") else dev(v)) for k, v in inp.items()}
+    out = lbm_selective_scan_fwd(**t, **kw)
+    if isinstance(out, tuple):
+        return tuple(o.float().cpu().numpy() for o in out)
+    return out.float().cpu().numpy()
+
+
+def quantize(inp, dtype):
+    """Round the sequence inputs to ``dtype`` so the oracle sees what the GPU sees."""
+    return {k: (dev(v, dtype).float().cpu().numpy().astype(np.float64)
+                if k in ("u", "delta", "z", "B", "C") else v) for k, v in inp.items()}
+
+
+# --- fused operator -----------------------------------------------------------
+
+@pytest.mark.parametrize("L", [1, 5, 31, 128, 129, 197, 256, 257])
+@pytest.mark.parametrize("M", [1, 3, 4, 8, 16])
+@pytest.mark.parametrize("reverse", [False, True])
+def test_fused_fp32_grid(L, M, reverse):
+    inp = op_inputs(100 + L + M, 2, L, 5, 4)
+    got = run_gpu(inp, window=M, reverse=reverse)
+    ref = O.lbm_selective_scan(**inp, window=M, reverse=reverse)
+    assert O.max_rel_err(got, ref) <= TOL_F32
+
+
+@pytest.mark.parametrize("N", [1, 3, 4, 7, 8, 16])
+def test_fused_state_sizes(N):
+    inp = op_inputs(7 + N, 2, 97, 37, N)
+    got, hf = run_gpu(inp, window=8, return_last_state=True)
+    ref, rhf = O.lbm_selective_scan(**inp, window=8, return_last_state=True)
+    assert O.max_rel_err(got, ref) <= TOL_F32
+    assert O.max_rel_err(hf, rhf) <= TOL_F32
+
+
+def test_cfg1_shape_fp32():
+    """BASELINE configs[0]: B=2 D=192 L=197 N=16 window 8, fp32."""
+    inp = op_inputs(0, 2, 197, 192, 16, random_A=False)
+    for reverse in (False, True):
+        got, hf = run_gpu(inp, window=8, reverse=reverse, return_last_state=True)
+        ref, rhf = O.lbm_selective_scan(**inp, window=8, reverse=reverse, return_last_state=True)
+        assert O.max_rel_err(got, ref) <= TOL_F32
+        assert O.max_rel_err(hf, rhf) <= TOL_F32
+
+
+@pytest.mark.parametrize("reverse", [False, True])
+def test_fused_bf16(reverse):
+    inp = quantize(op_inputs(3, 4, 197, 384, 16, random_A=False), torch.bfloat16)
+    got = run_gpu(inp, dtype=torch.bfloat16, window=8, reverse=reverse)
+    ref = O.lbm_selective_scan(**inp, window=8, reverse=reverse)
+    assert O.max_rel_err(got, ref) <= TOL_BF16
+
+
+def test_optional_inputs_and_modes():
+    inp = op_inputs(11, 2, 50, 9, 4)
+    for drop in ("z", "D", "delta_bias"):
+        x = dict(inp)
+        x[drop] = None
+        got = run_gpu({k: v for k, v in x.items() if v is not None}, window=4)
+        ref = O.lbm_selective_scan(**x, window=4)
+        assert O.max_rel_err(got, ref) <= TOL_F32, drop
+    # without softplus the step must already be positive for a contractive decay
+    x = dict(inp)
+    x["delta"] = np.abs(inp["delta"]) * 0.2
+    x["delta_bias"] = np.abs(inp["delta_bias"]) * 0.01
+    got = run_gpu(x, window=4, delta_softplus=False)
+    ref = O.lbm_selective_scan(**x, window=4, delta_softplus=False)
+    assert O.max_rel_err(got, ref) <= TOL_F32
+    # discretize_mode="linear" (block.py:94) with a contractive decay
+    x = dict(inp)
+    x["A"] = -np.abs(inp["A"]) * 0.05
+    got = run_gpu(x, window=4, discretize_mode="linear")
+    ref = O.lbm_selective_scan(**x, window=4, mode="linear")
+    assert O.max_rel_err(got, ref) <= TOL_F32
+
+
+def test_window_longer_than_sequence_is_one_tile():
+    inp = op_inputs(5, 1, 5, 3, 4)
+    a = run_gpu(inp, window=16)
+    b = run_gpu(inp, window=5)
+    np.testing.assert_array_equal(a, b)
+    assert O.max_rel_err(a, O.lbm_selective_scan(**inp, window=5)) <= TOL_F32
+
+
+def test_m1_equals_forward_bitwise_and_tile_ends():
+    """test_engine.py:98-114 on the fused kernel: LB with M=1 and LB outputs at
+    tile ends are bitwise the forward-only scan's."""
+    inp = op_inputs(21, 2, 61, 40, 16)
+    t = {k: dev(v) for k, v in inp.items()}
+    fwd = selective_scan(**t).cpu().numpy()
+    m1 = lbm_selective_scan(**t, window=1).cpu().numpy()
+    np.testing.assert_array_equal(m1, fwd)
+    for M in (3, 4, 8, 16):
+        lb = lbm_selective_scan(**t, window=M).cpu().numpy()
+        for i in range(61):
+            if (i + 1) % M == 0 or i == 60:
+                np.testing.assert_array_equal(lb[:, i], fwd[:, i])
+    assert O.max_rel_err(fwd, O.lbm_selective_scan(**inp, window=1)) <= TOL_F32
+
+
+@pytest.mark.parametrize("S", [2, 3, 7])
+def test_sequence_split_matches_unsplit(S):
+    inp = op_inputs(33, 2, 777, 70, 16)
+    for reverse in (False, True):
+        got, hf = run_gpu(inp, window=16, reverse=reverse, return_last_state=True, seg_hint=S)
+        ref, rhf = O.lbm_selective_scan(**inp, window=16, reverse=reverse, return_last_state=True)
+        assert O.max_rel_err(got, ref) <= TOL_F32
+        assert O.max_rel_err(hf, rhf) <= TOL_F32
+
+
+def test_long_sequence_auto_split_fp32():
+    """cfg-5-like: few channels, long L -> the launcher splits L; compare a
+    (b, e) subsample with the oracle (lanes are independent, so exact)."""
+    inp = op_inputs(44, 1, 20000, 64, 16)
+    got = run_gpu(inp, window=16)
+    sub = {k: (v[:, :, :8] if k in ("u", "delta", "z") else v[:8] if k in ("A", "D", "delta_bias") else v)
+           for k, v in inp.items()}
+    ref = O.lbm_selective_scan(**sub, window=16)
+    assert O.max_rel_err(got[:, :, :8], ref) <= TOL_F32
+
+
+def test_strided_views_of_fused_projection():
+    """B and C as column slices of one (B, L, E+2N) projection output, u as a
+    transposed view: strides go straight to the kernel, no copies."""
+    inp = op_inputs(9, 2, 64, 24, 16)
+    Bt, L, E = inp["u"].shape
+    proj = np.concatenate([inp["delta"], inp["B"], inp["C"]], axis=-1)
+    P = dev(proj)
+    uT = dev(np.ascontiguousarray(inp["u"].transpose(0, 2, 1))).transpose(1, 2)
+    got = lbm_selective_scan(uT, P[..., :E], dev(inp["A"]), P[..., E:E + 16], P[..., E + 16:],
+                             D=dev(inp["D"]), z=dev(inp["z"]), delta_bias=dev(inp["delta_bias"]),
+                             window=4).cpu().numpy()
+    ref = O.lbm_selective_scan(**inp, window=4)
+    assert O.max_rel_err(got, ref) <= TOL_F32
+
+
+# --- pre-discretised entry: the reference's own grid and fixtures ---------------
+
+@pytest.fixture(scope="module")
+def grid():
+    return np.load(os.path.join(GOLD, "scan_grid.npz"))
+
+
+@pytest.mark.parametrize("L", [1, 5, 31, 128, 129, 197, 256, 257])
+def test_prediscretized_grid_vs_reference(grid, L):
+    p = [grid[f"L{L}_{k}"] for k in ("abar", "bx", "c", "dx")]
+    p32 = [a.astype(np.float32) for a in p]
+    for M in (1, 3, 4, 8, 16):
+        plan = TilePlan.for_length(L, M)
+        ref = grid[f"L{L}_M{M}_lbm_y"]
+        g64 = engine.lbm_scan_par(*p, plan)
+        assert O.max_rel_err(g64.y, ref) <= 1e-12
+        assert O.max_rel_err(g64.h_final, grid[f"L{L}_fwd_h"]) <= 1e-12
+        g32 = engine.lbm_scan_par(*p32, plan)
+        assert O.max_rel_err(g32.y, ref) <= TOL_F32
+        rv = engine.lbm_scan_par_reverse(*p, plan)
+        assert O.max_rel_err(rv.y, grid[f"L{L}_M{M}_rev_y"]) <= 1e-12
+        assert O.max_rel_err(rv.h_final, grid[f"L{L}_M{M}_rev_h"]) <= 1e-12
+    f = engine.forward_scan_par(*p, TilePlan.for_length(L, 4))
+    assert O.max_rel_err(f.y, grid[f"L{L}_fwd_y"]) <= 1e-12
+
+
+def test_prediscretized_bitwise_identities():
+    """test_engine.py:98-114, fp64."""
+    p = O.random_scan_params(O.seeded_rng(12), 2, 29, 2, 3)
+    fwd = engine.forward_scan_par(*p, TilePlan.for_length(29, 4))
+    lbm = engine.lbm_scan_par(*p, TilePlan.for_length(29, 4))
+    for i in range(29):
+        if (i + 1) % 4 == 0 or i == 28:
+            np.testing.assert_array_equal(lbm.y[:, i], fwd.y[:, i])
+    m1 = engine.lbm_scan_par(*p, TilePlan.for_length(29, 1))
+    np.testing.assert_array_equal(m1.y, engine.forward_scan_par(*p, TilePlan.for_length(29, 1)).y)
+
+
+def test_prediscretized_large_window_and_bidir():
+    p = O.random_scan_params(O.seeded_rng(3), 2, 300, 3, 4)
+    got = engine.lbm_scan_par(*p, TilePlan.for_length(300, 100))
+    assert O.max_rel_err(got.y, O.lbm_scan(*p, 100)[0]) <= 1e-12
+    pb = O.random_scan_params(O.seeded_rng(4), 2, 300, 3, 4)
+    bid = engine.global_bidir_par(p, pb, TilePlan.for_length(300, 8))
+    ry, rh = O.global_bidir_scan(p, pb)
+    assert O.max_rel_err(bid.y, ry) <= 1e-12
+    assert O.max_rel_err(bid.h_final, rh) <= 1e-12
+
+
+def test_plan_consistency_checked():
+    from paper_2506_15976_b200.errors import ShapeError
+    p = O.random_scan_params(O.seeded_rng(0), 1, 8, 2, 2, dtype=np.float32)
+    with pytest.raises(ShapeError):
+        engine.forward_scan_par(*p, TilePlan(tile_len=4, num_tiles=7))
+
+
+# --- conv ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("reverse", [False, True])
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_conv_fwd_bwd(reverse, K):
+    from paper_2506_15976_b200.conv import causal_conv1d_silu_bwd, causal_conv1d_silu_fwd
+    rng = O.seeded_rng(K + 10 * reverse)
+    x = rng.standard_normal((2, 77, 50))
+    w = rng.standard_normal((50, K)) * 0.5
+    g = rng.standard_normal((2, 77, 50))
+    flip = (lambda a: a[:, ::-1]) if reverse else (lambda a: a)
+    xc = O.causal_conv1d(flip(x), w)
+    ref = flip(O.silu(xc))
+    got = causal_conv1d_silu_fwd(dev(x), dev(w), reverse=reverse).cpu().numpy()
+    assert O.max_rel_err(got, ref) <= TOL_F32
+    gx_ref, gw_ref = O.causal_conv1d_grad(flip(x), w, flip(g) * O.silu_grad(xc))
+    dx, dw, _ = causal_conv1d_silu_bwd(dev(x), dev(w), None, dev(g), reverse=reverse)
+    assert O.max_rel_err(dx.cpu().numpy(), flip(gx_ref)) <= TOL_F32
+    assert O.max_rel_err(dw.cpu().numpy(), gw_ref) <= TOL_F32
+
+
+def test_conv_golden():
+    from paper_2506_15976_b200.conv import causal_conv1d_silu_bwd, causal_conv1d_silu_fwd
+    g = np.load(os.path.join(GOLD, "conv.npz"))
+    y = causal_conv1d_silu_fwd(dev(g["x"]), dev(g["k"]), silu=False).cpu().numpy()
+    assert O.max_rel_err(y, g["y"]) <= TOL_F32
+    dx, dw, _ = causal_conv1d_silu_bwd(dev(g["x"]), dev(g["k"]), None, dev(g["g"]), silu=False)
+    assert O.max_rel_err(dx.cpu().numpy(), g["gx"]) <= TOL_F32
+    assert O.max_rel_err(dw.cpu().numpy(), g["gk"]) <= TOL_F32
