@@ -33,8 +33,8 @@ bool io_dtype_ok(int d) { return d == LBS_F32 || d == LBS_BF16 || d == LBS_F16; 
 
 constexpr int kNumSMs = 148;
 
-// states padded per thread (kernels instantiate NS in {4, 8, 16})
-int padded_states(int64_t N) { return N <= 4 ? 4 : (N <= 8 ? 8 : 16); }
+// states padded per thread (kernels instantiate NS in {4, 16})
+int padded_states(int64_t N) { return N <= 4 ? 4 : 16; }
 
 // Sequence-split plan: cut L into S segments (multiples of the window) only
 // when B*E alone cannot fill the machine; each extra segment costs one extra
@@ -73,6 +73,13 @@ int validate_fwd(const lbs_scan_fwd_args* a) {
     return fail(LBS_ERR_UNSUPPORTED, "sequence or channel count too large");
   if (!io_dtype_ok(a->io_dtype)) return fail(LBS_ERR_INVALID, "bad io dtype %d", a->io_dtype);
   if (!io_dtype_ok(a->bc_dtype)) return fail(LBS_ERR_INVALID, "bad B/C dtype %d", a->bc_dtype);
+  {
+    const bool ok = (a->io_dtype == LBS_F32 && a->bc_dtype == LBS_F32) ||
+                    (a->io_dtype == LBS_BF16 && (a->bc_dtype == LBS_BF16 || a->bc_dtype == LBS_F32));
+    if (!ok)
+      return fail(LBS_ERR_UNSUPPORTED, "dtype combination io=%d bc=%d not instantiated (f32/f32, bf16/bf16, bf16/f32)",
+                  a->io_dtype, a->bc_dtype);
+  }
   if (!a->u || !a->delta || !a->A || !a->B || !a->C || !a->out)
     return fail(LBS_ERR_INVALID, "u, delta, A, B, C and out must be non-null");
   if (a->dstate > 16)

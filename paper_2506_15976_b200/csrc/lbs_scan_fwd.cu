@@ -1,487 +1,17 @@
-// Fused LB selective scan — forward (sm_100a).
-//
-// Replaces, in one launch, the reference's numpy discretisation
-// (block._discretize_cached, block.py:87-103 — materialises two (B,L,E,N)
-// tensors), the numba tiled scan (engine._scan_kernel, engine.py:88-218), the
-// D-skip and the SiLU(z) gate (block.py:177-178).  Nothing of size (B,L,E,N)
-// ever touches HBM: per (b,l) the kernel reads u, delta, z (E each) and B, C
-// (N each) and writes out (E).
-//
-// Execution model (B200-first, not the reference's 3-phase tile scan):
-//  * one thread owns one (b, e) channel and ALL its N states, and sweeps the
-//    sequence serially: the forward recurrence costs 1 FFMA per state-step
-//    (no in-tile aggregate + rescan as in engine.py:128-154).  The LB window
-//    of M steps lives in registers: per tile the thread first runs the
-//    tile-local backward recurrence r_i = a_i (r_{i+1} + b_{i+1})
-//    (oracle.py:80-112) accumulating C_i·r_i into the outputs, then the
-//    forward recurrence h_i = a_i h_{i-1} + b_i accumulating C_i·h_i.
-//  * state pairs (n, n+1) use packed FFMA2/FMUL2/FADD2; exp(delta*A) is one
-//    MUFU.EX2 per state-step — the kernel is MUFU/issue-bound.
-//  * a CTA owns 128 consecutive channels of one batch row.  Chunks of CL steps
-//    of u/delta/z are staged into a 2-stage shared-memory ring with cp.async
-//    (16-byte LDGSTS, coalesced rows) one chunk ahead of the compute; B and C
-//    of the chunk (shared by all channels) are prefetched into registers one
-//    chunk ahead and published to shared memory as fp32, so the warp reads
-//    them as broadcast LDS.64.  Global-memory latency is off the critical path.
-//  * reverse direction = flip-on-load: the stager copies physical row
-//    L-1-t into ring row t, so the compute loop is direction-agnostic and
-//    tiles are aligned from logical 0 (engine.py:133,183).
-//  * optional sequence split (long L, few channels): pass 1
-//    (segment_state_kernel) computes each segment's affine aggregate
-//    h -> P h + H per lane; the main pass enters segment s with the exact
-//    state folded from segments < s.  Segment boundaries are tile boundaries.
-#include "lbs_common.cuh"
+// Fused LB selective scan forward: dtype dispatch (kernels in lbs_scan_fwd.cuh,
+// one instantiation unit per dtype combination so nvcc runs them in parallel).
 #include "lbs_internal.h"
+#include "../../include/lbscan_b200.h"
 
 namespace lbs {
-
-// ---------------------------------------------------------------------------
-// cp.async helpers
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
-template <typename Tio>
-struct FwdCfg {
-  static constexpr int CL = sizeof(Tio) == 4 ? 16 : 32;   // max steps per chunk
-  static constexpr int PPR = kFwdThreads * sizeof(Tio) / 16;  // 16-byte pieces per row
-};
-
-// Shared-memory layout (dynamic):
-//   seq[2 stages][3 arrays][CL][128]  (Tio)   u, delta, z
-//   bcf[CL][2*NS]                      (f32)   B then C per step, zero padded
-//   a2s[NS/2][128]                     (f2)    A*log2(e) per channel pair
-template <typename Tio, int NS>
-struct FwdSmem {
-  static constexpr int CL = FwdCfg<Tio>::CL;
-  static constexpr size_t seq_bytes = 2ull * 3 * CL * kFwdThreads * sizeof(Tio);
-  static constexpr size_t bc_bytes = (size_t)CL * 2 * NS * sizeof(float);
-  static constexpr size_t a2_bytes = (size_t)(NS / 2) * kFwdThreads * sizeof(f2);
-  static constexpr size_t total = seq_bytes + bc_bytes + a2_bytes;
-};
-
-// Stage the sequence rows of logical steps [c, c+clen) into ring stage `st`.
-template <typename Tio, bool kVec>
-__device__ __forceinline__ void stage_seq(const FwdParams& p, Tio* seq, int st, int c, int clen,
-                                          int b, int e0, bool has_z) {
-  constexpr int CL = FwdCfg<Tio>::CL;
-  const int L = p.L;
-  const bool rev = p.flags & LBS_FLAG_REVERSE;
-  if constexpr (kVec) {
-    constexpr int PPR = FwdCfg<Tio>::PPR;
-    constexpr int EPP = 16 / sizeof(Tio);  // elements per piece
-    const int narr = has_z ? 3 : 2;
-    const int total = narr * clen * PPR;
-    for (int idx = threadIdx.x; idx < total; idx += kFwdThreads) {
-      const int arr = idx / (clen * PPR);
-      const int rem = idx - arr * clen * PPR;
-      const int t = rem / PPR;
-      const int pc = rem - t * PPR;
-      const int e = e0 + pc * EPP;
-      if (e < p.E) {
-        const View3D& v = arr == 0 ? p.u : (arr == 1 ? p.delta : p.z);
-        const long long pl = rev ? (L - 1 - (c + t)) : (c + t);
-        const Tio* g = static_cast<const Tio*>(v.p) + (long long)b * v.s0 + pl * v.s1 + (long long)e * v.s2;
-        Tio* s = seq + (((size_t)st * 3 + arr) * CL + t) * kFwdThreads + pc * EPP;
-        cp_async16(s, g);
-      }
-    }
-  } else {
-    const int narr = has_z ? 3 : 2;
-    for (int arr = 0; arr < narr; ++arr) {
-      const View3D& v = arr == 0 ? p.u : (arr == 1 ? p.delta : p.z);
-      const int e = e0 + threadIdx.x;
-      if (e >= p.E) continue;
-      for (int t = 0; t < clen; ++t) {
-        const long long pl = rev ? (L - 1 - (c + t)) : (c + t);
-        const Tio* g = static_cast<const Tio*>(v.p) + (long long)b * v.s0 + pl * v.s1 + (long long)e * v.s2;
-        seq[(((size_t)st * 3 + arr) * CL + t) * kFwdThreads + threadIdx.x] = *g;
-      }
-    }
-  }
-}
-
-// B/C of one chunk: each thread fetches up to BCR values into registers.
-template <typename Tbc, int NS, int CL>
-struct BcPrefetch {
-  static constexpr int BCR = (CL * 2 * NS + kFwdThreads - 1) / kFwdThreads;
-  float v[BCR];
-  __device__ __forceinline__ void load(const FwdParams& p, const Tbc* Bp, const Tbc* Cp, int c, int clen) {
-    const int L = p.L;
-    const bool rev = p.flags & LBS_FLAG_REVERSE;
-#pragma unroll
-    for (int k = 0; k < BCR; ++k) {
-      const int idx = threadIdx.x + k * kFwdThreads;
-      const int t = idx / (2 * NS);
-      const int kk = idx - t * (2 * NS);
-      const int which = kk / NS;
-      const int n = kk - which * NS;
-      float x = 0.f;
-      if (t < clen && n < p.N) {
-        const long long pl = rev ? (L - 1 - (c + t)) : (c + t);
-        x = which == 0 ? ld<Tbc>(Bp + pl * p.Bm.s1 + (long long)n * p.Bm.s2)
-                       : ld<Tbc>(Cp + pl * p.Cm.s1 + (long long)n * p.Cm.s2);
-      }
-      v[k] = x;
-    }
-  }
-  __device__ __forceinline__ void publish(float* bcf) const {
-#pragma unroll
-    for (int k = 0; k < BCR; ++k) {
-      const int idx = threadIdx.x + k * kFwdThreads;
-      if (idx < CL * 2 * NS) bcf[idx] = v[k];
-    }
-  }
-};
-
-// One LB tile of r steps at ring rows [t0, t0+r): all state pairs, then the
-// D-skip + gate + store.  For MT > 8 the injections b_j are recomputed in the
-// forward sweep instead of held (keeps the 16-step window under 168 regs).
-struct TileOut {
-  void* op;
-  long long so1;
-  int L, c;
-  bool rev, active, has_z;
-  float Dv;
-};
-
-template <typename Tio, int NS, int MT, bool kLB, bool kFull>
-__device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const Tio* sz,
-                                             const float* bcf, const f2* a2s, f2 (&h)[NS / 2],
-                                             int t0, int r, float bias, bool softplus, bool linear,
-                                             const TileOut& o) {
-  constexpr int NP = NS / 2;
-  constexpr bool kHoldB = MT <= 8;
-  const int tid = threadIdx.x;
-  float dl[MT], du[MT];
-  f2 yacc[MT];
-#pragma unroll
-  for (int j = 0; j < MT; ++j) {
-    const bool on = kFull || j < r;
-    float d = on ? to_f(sd[(t0 + j) * kFwdThreads + tid]) + bias : 0.f;
-    const float uv = on ? to_f(su[(t0 + j) * kFwdThreads + tid]) : 0.f;
-    if (softplus) d = softplus_f(d);
-    dl[j] = d;
-    du[j] = d * uv;
-    yacc[j] = mk2(o.Dv * uv, 0.f);  // D-skip folded into the accumulator
-  }
-#pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    const f2 A2 = a2s[q * kFwdThreads + tid];
-    f2 a[MT], bb[kHoldB ? MT : 1];
-#pragma unroll
-    for (int j = 0; j < MT; ++j) {
-      const f2 x = mul2(bc2(dl[j]), A2);
-      a[j] = linear ? x : mk2(ex2(x.x), ex2(x.y));
-      if constexpr (kHoldB) {
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + 2 * q]);
-        bb[j] = mul2(bc2(du[j]), Bv);
-      }
-    }
-    auto binj = [&](int j) -> f2 {
-      if constexpr (kHoldB) {
-        return bb[j];
-      } else {
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + 2 * q]);
-        return mul2(bc2(du[j]), Bv);
-      }
-    };
-    if (kLB) {
-      // exclusive tile-local backward record: r_{end} = 0, r_i = a_i (r_{i+1} + b_{i+1})
-      f2 s = mk2(0.f, 0.f);
-#pragma unroll
-      for (int j = MT - 1; j >= 0; --j) {
-        if (kFull ? (j == MT - 1) : (j == r - 1)) {
-          s = binj(j);
-        } else if (kFull || j < r - 1) {
-          const f2 rr = mul2(a[j], s);
-          const f2 Cv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + NS + 2 * q]);
-          yacc[j] = fma2(Cv, rr, yacc[j]);
-          s = add2(rr, binj(j));
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < MT; ++j) {
-      if (kFull || j < r) {
-        h[q] = fma2(a[j], h[q], binj(j));
-        const f2 Cv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + NS + 2 * q]);
-        yacc[j] = fma2(Cv, h[q], yacc[j]);
-      }
-    }
-  }
-  if (o.active) {
-    Tio* op = static_cast<Tio*>(o.op);
-#pragma unroll
-    for (int j = 0; j < MT; ++j) {
-      if (kFull || j < r) {
-        float y = yacc[j].x + yacc[j].y;
-        if (o.has_z) y *= silu_f(to_f(sz[(t0 + j) * kFwdThreads + tid]));
-        const long long pl = o.rev ? (o.L - 1 - (o.c + t0 + j)) : (o.c + t0 + j);
-        st<Tio>(op + pl * o.so1, y);
-      }
-    }
-  }
-}
-
-template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec>
-__global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? 4 : 2)) fwd_kernel(FwdParams p) {
-  constexpr int NP = NS / 2;
-  constexpr int CL = FwdCfg<Tio>::CL;
-  using Sm = FwdSmem<Tio, NS>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Tio* seq = reinterpret_cast<Tio*>(smem_raw);
-  float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
-  f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
-
-  const int tid = threadIdx.x;
-  const int e0 = blockIdx.x * kFwdThreads;
-  const int e = e0 + tid;
-  const int b = blockIdx.y;
-  const int seg = blockIdx.z;
-  const bool active = e < p.E;
-  const int ec = active ? e : p.E - 1;
-  const int L = p.L, N = p.N, m = p.m;
-  const bool rev = p.flags & LBS_FLAG_REVERSE;
-  const bool softplus = p.flags & LBS_FLAG_SOFTPLUS;
-  const bool linear = p.flags & LBS_FLAG_LINEAR;
-  const bool has_z = p.z.p != nullptr;
-  const int CLm = (CL / m) * m;  // steps per chunk: whole tiles
-  const int seg_lo = seg * p.seg_len;
-  const int seg_hi = min(L, seg_lo + p.seg_len);
-
-#pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    float a0 = 2 * q < N ? p.A[(long long)ec * N + 2 * q] : 0.f;
-    float a1 = 2 * q + 1 < N ? p.A[(long long)ec * N + 2 * q + 1] : 0.f;
-    if (!linear) { a0 *= kLog2e; a1 *= kLog2e; }
-    a2s[q * kFwdThreads + tid] = mk2(a0, a1);
-  }
-  const float Dv = p.D ? p.D[ec] : 0.f;
-  const float bias = p.bias ? p.bias[ec] : 0.f;
-
-  f2 h[NP];
-#pragma unroll
-  for (int q = 0; q < NP; ++q) h[q] = mk2(0.f, 0.f);
-  if (seg > 0) {
-    const float* agg = p.seg_agg;
-    for (int s = 0; s < seg; ++s) {
-      const f2* PH = reinterpret_cast<const f2*>(agg + ((((long long)b * p.n_seg + s) * p.E + ec) * (2 * NS)));
-#pragma unroll
-      for (int q = 0; q < NP; ++q) h[q] = fma2(PH[q], h[q], PH[NP + q]);
-    }
-  }
-
-  Tio* op = static_cast<Tio*>(p.out) + (long long)b * p.so0 + (long long)ec * p.so2;
-  const Tbc* Bp = static_cast<const Tbc*>(p.Bm.p) + (long long)b * p.Bm.s0;
-  const Tbc* Cp = static_cast<const Tbc*>(p.Cm.p) + (long long)b * p.Cm.s0;
-
-  BcPrefetch<Tbc, NS, CL> bcpre;
-  // prologue: chunk 0
-  int c = seg_lo;
-  int clen = min(CLm, seg_hi - c);
-  stage_seq<Tio, kVec>(p, seq, 0, c, clen, b, e0, has_z);
-  cp_async_commit();
-  bcpre.load(p, Bp, Cp, c, clen);
-
-  for (int k = 0; c < seg_hi; ++k) {
-    const int stg = k & 1;
-    const int cn = c + clen;
-    const int clen_n = cn < seg_hi ? min(CLm, seg_hi - cn) : 0;
-    cp_async_wait_all();
-    __syncthreads();  // chunk k landed (all threads); compute of chunk k-1 done
-    bcpre.publish(bcf);
-    if (clen_n > 0) {
-      stage_seq<Tio, kVec>(p, seq, stg ^ 1, cn, clen_n, b, e0, has_z);
-      bcpre.load(p, Bp, Cp, cn, clen_n);
-    }
-    cp_async_commit();
-    __syncthreads();  // bcf visible
-
-    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * kFwdThreads;
-    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * kFwdThreads;
-    const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * kFwdThreads;
-    const TileOut o{op, p.so1, L, c, rev, active, has_z, Dv};
-    for (int t0 = 0; t0 < clen; t0 += m) {
-      const int r = min(m, clen - t0);
-      if (r == MT)
-        tile_compute<Tio, NS, MT, kLB, true>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
-      else
-        tile_compute<Tio, NS, MT, kLB, false>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
-    }
-    c = cn;
-    clen = clen_n;
-  }
-
-  if (active && p.last_state && seg_hi == L) {
-    float* hs = p.last_state + ((long long)b * p.E + e) * N;
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      if (2 * q < N) hs[2 * q] = h[q].x;
-      if (2 * q + 1 < N) hs[2 * q + 1] = h[q].y;
-    }
-  }
-}
-
-// Pass 1 of the sequence split: per (b, segment, e, n) the segment's
-// aggregate affine map h -> P*h + H with P = prod a = exp(A * sum delta) and
-// H the local end state from zero (core.py:48-55 combine, applied serially).
-template <typename Tio, typename Tbc, int NS, bool kVec>
-__global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p) {
-  constexpr int NP = NS / 2;
-  constexpr int CL = FwdCfg<Tio>::CL;
-  using Sm = FwdSmem<Tio, NS>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Tio* seq = reinterpret_cast<Tio*>(smem_raw);
-  float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
-  f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
-
-  const int tid = threadIdx.x;
-  const int e0 = blockIdx.x * kFwdThreads;
-  const int e = e0 + tid;
-  const int b = blockIdx.y;
-  const int seg = blockIdx.z;
-  const bool active = e < p.E;
-  const int ec = active ? e : p.E - 1;
-  const int L = p.L, N = p.N;
-  const bool softplus = p.flags & LBS_FLAG_SOFTPLUS;
-  const bool linear = p.flags & LBS_FLAG_LINEAR;
-  const int seg_lo = seg * p.seg_len;
-  const int seg_hi = min(L, seg_lo + p.seg_len);
-  (void)L;
-
-#pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    float a0 = 2 * q < N ? p.A[(long long)ec * N + 2 * q] : 0.f;
-    float a1 = 2 * q + 1 < N ? p.A[(long long)ec * N + 2 * q + 1] : 0.f;
-    if (!linear) { a0 *= kLog2e; a1 *= kLog2e; }
-    a2s[q * kFwdThreads + tid] = mk2(a0, a1);
-  }
-  const float bias = p.bias ? p.bias[ec] : 0.f;
-  const Tbc* Bp = static_cast<const Tbc*>(p.Bm.p) + (long long)b * p.Bm.s0;
-  const Tbc* Cp = static_cast<const Tbc*>(p.Cm.p) + (long long)b * p.Cm.s0;
-
-  f2 H[NP], P[NP];
-#pragma unroll
-  for (int q = 0; q < NP; ++q) { H[q] = mk2(0.f, 0.f); P[q] = mk2(1.f, 1.f); }
-  float dsum = 0.f;
-
-  BcPrefetch<Tbc, NS, CL> bcpre;
-  int c = seg_lo;
-  int clen = min(CL, seg_hi - c);
-  stage_seq<Tio, kVec>(p, seq, 0, c, clen, b, e0, false);
-  cp_async_commit();
-  bcpre.load(p, Bp, Cp, c, clen);
-  for (int k = 0; c < seg_hi; ++k) {
-    const int stg = k & 1;
-    const int cn = c + clen;
-    const int clen_n = cn < seg_hi ? min(CL, seg_hi - cn) : 0;
-    cp_async_wait_all();
-    __syncthreads();
-    bcpre.publish(bcf);
-    if (clen_n > 0) {
-      stage_seq<Tio, kVec>(p, seq, stg ^ 1, cn, clen_n, b, e0, false);
-      bcpre.load(p, Bp, Cp, cn, clen_n);
-    }
-    cp_async_commit();
-    __syncthreads();
-    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * kFwdThreads;
-    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * kFwdThreads;
-    for (int t = 0; t < clen; ++t) {
-      float dl = to_f(sd[t * kFwdThreads + tid]) + bias;
-      if (softplus) dl = softplus_f(dl);
-      const float du = dl * to_f(su[t * kFwdThreads + tid]);
-      dsum += dl;
-#pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        const f2 x = mul2(bc2(dl), a2s[q * kFwdThreads + tid]);
-        const f2 a = linear ? x : mk2(ex2(x.x), ex2(x.y));
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[t * 2 * NS + 2 * q]);
-        H[q] = fma2(a, H[q], mul2(bc2(du), Bv));
-        if (linear) P[q] = mul2(P[q], a);
-      }
-    }
-    c = cn;
-    clen = clen_n;
-  }
-  if (!linear) {
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      const f2 x = mul2(bc2(dsum), a2s[q * kFwdThreads + tid]);
-      P[q] = mk2(ex2(x.x), ex2(x.y));
-    }
-  }
-  if (active) {
-    f2* out = reinterpret_cast<f2*>(p.seg_agg + ((((long long)b * p.n_seg + seg) * p.E + e) * (2 * NS)));
-#pragma unroll
-    for (int q = 0; q < NP; ++q) { out[q] = P[q]; out[NP + q] = H[q]; }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// launcher
-
-template <typename Tio, typename Tbc, int NS, int MT, bool kVec>
-static cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
-  const size_t smem = FwdSmem<Tio, NS>::total;
-  dim3 block(kFwdThreads);
-  if (p.n_seg > 1) {
-    auto k1 = segment_state_kernel<Tio, Tbc, NS, kVec>;
-    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 g1((p.E + kFwdThreads - 1) / kFwdThreads, p.Bt, p.n_seg - 1);
-    k1<<<g1, block, smem, st>>>(p);
-  }
-  dim3 grid((p.E + kFwdThreads - 1) / kFwdThreads, p.Bt, p.n_seg);
-  auto k = (p.flags & LBS_FLAG_LB) ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec>
-                                   : fwd_kernel<Tio, Tbc, NS, MT, false, kVec>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<grid, block, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-template <typename Tio, typename Tbc, int NS, bool kVec>
-static cudaError_t launch_fwd_m(const FwdParams& p, cudaStream_t st) {
-  if (p.m <= 1) return launch_fwd_t<Tio, Tbc, NS, 1, kVec>(p, st);
-  if (p.m <= 2) return launch_fwd_t<Tio, Tbc, NS, 2, kVec>(p, st);
-  if (p.m <= 4) return launch_fwd_t<Tio, Tbc, NS, 4, kVec>(p, st);
-  if (p.m <= 8) return launch_fwd_t<Tio, Tbc, NS, 8, kVec>(p, st);
-  return launch_fwd_t<Tio, Tbc, NS, 16, kVec>(p, st);
-}
-
-template <typename Tio, typename Tbc, bool kVec>
-static cudaError_t launch_fwd_n(const FwdParams& p, cudaStream_t st) {
-  if (p.N <= 4) return launch_fwd_m<Tio, Tbc, 4, kVec>(p, st);
-  if (p.N <= 8) return launch_fwd_m<Tio, Tbc, 8, kVec>(p, st);
-  return launch_fwd_m<Tio, Tbc, 16, kVec>(p, st);
-}
-
-// 16-byte cp.async staging needs 16-byte aligned rows of whole pieces
-template <typename Tio>
-static bool vec_ok(const FwdParams& p) {
-  const size_t es = sizeof(Tio);
-  const int epp = 16 / (int)es;
-  auto ok = [&](const View3D& v) {
-    if (!v.p) return true;
-    return v.s2 == 1 && (reinterpret_cast<uintptr_t>(v.p) % 16) == 0 && (v.s0 * es) % 16 == 0 &&
-           (v.s1 * es) % 16 == 0;
-  };
-  return p.E % epp == 0 && ok(p.u) && ok(p.delta) && ok(p.z);
-}
-
-template <typename Tio, typename Tbc>
-static cudaError_t launch_fwd_v(const FwdParams& p, cudaStream_t st) {
-  return vec_ok<Tio>(p) ? launch_fwd_n<Tio, Tbc, true>(p, st) : launch_fwd_n<Tio, Tbc, false>(p, st);
-}
+cudaError_t launch_fwd_f32(const FwdParams& p, cudaStream_t st);
+cudaError_t launch_fwd_bf16(const FwdParams& p, cudaStream_t st);
+cudaError_t launch_fwd_bf16f32(const FwdParams& p, cudaStream_t st);
 
 cudaError_t launch_fwd(const FwdParams& p, int io_dtype, int bc_dtype, cudaStream_t st) {
-  if (io_dtype == LBS_F32 && bc_dtype == LBS_F32) return launch_fwd_v<float, float>(p, st);
-  if (io_dtype == LBS_BF16 && bc_dtype == LBS_BF16) return launch_fwd_v<__nv_bfloat16, __nv_bfloat16>(p, st);
-  if (io_dtype == LBS_BF16 && bc_dtype == LBS_F32) return launch_fwd_v<__nv_bfloat16, float>(p, st);
-  if (io_dtype == LBS_F16 && bc_dtype == LBS_F16) return launch_fwd_v<__half, __half>(p, st);
+  if (io_dtype == LBS_F32 && bc_dtype == LBS_F32) return launch_fwd_f32(p, st);
+  if (io_dtype == LBS_BF16 && bc_dtype == LBS_BF16) return launch_fwd_bf16(p, st);
+  if (io_dtype == LBS_BF16 && bc_dtype == LBS_F32) return launch_fwd_bf16f32(p, st);
   return cudaErrorInvalidValue;
 }
-
 }  // namespace lbs

@@ -78,13 +78,13 @@ def _prepare(u, delta, A, B, C_, D, z, delta_bias, window):
     for name, t in (("B", B), ("C", C_)):
         if t.shape != (Bt, L, N):
             raise ShapeError(f"{name} has shape {tuple(t.shape)}, expected {(Bt, L, N)}")
-    if u.dtype not in _DT:
+    if u.dtype not in (torch.float32, torch.bfloat16):
         u = u.to(torch.float32)
     io = u.dtype
     delta = delta.to(io)
     if z is not None:
         z = z.to(io)
-    bc = B.dtype if B.dtype in _DT else torch.float32
+    bc = B.dtype if B.dtype in (torch.float32, torch.bfloat16) else torch.float32
     if bc != io and not (io == torch.bfloat16 and bc == torch.float32):
         bc = io
     B = B.to(bc)
@@ -179,5 +179,7 @@ def selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_sof
                    reverse=False, return_last_state=False):
     """Plain unidirectional selective scan (engine.forward_scan_par semantics,
     engine.py:294) — the same kernel with the LB pass compiled out."""
-    return lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 1,
+    # the window is irrelevant without the LB pass; 8-step tiles keep the
+    # forward-only kernel on its fast full-tile path
+    return lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8,
                                   reverse, return_last_state, False)
