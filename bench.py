@@ -1,0 +1,383 @@
+"""Benchmark: LBVim-Ti forward (BASELINE configs[1]) on the fused LB-scan kernels.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one LBVim-Ti forward (24 layers, dim 192, 224^2 patch 16, L=197,
+alternating scan direction) over a batch of 256 synthetic images in bf16 with
+fp32 scan state, random-init weights of the reference architecture.  N GPUs
+run one process each (torchrun) with the batch per GPU fixed (weak scaling,
+pure data parallel: no collective on the data path).
+
+Printed JSON (rank 0): ``value`` = images/s over all ranks, device-timed with
+CUDA events per step (L2 flushed between steps, outside the events), max over
+ranks; ``e2e`` = the same metric through the public API with pinned host
+images copied in and logits copied out every step (double-buffered on a copy
+stream); ``roofline`` = the fused scan kernel's algorithmic GB/s vs the
+measured HBM peak; ``cpu_baseline`` = the reference CPU path (oracle port:
+numpy + the engine restated in C/OpenMP, bitwise equal to the reference
+engine) on a bounded sample on this host.
+``--impl reference`` times only that CPU path (rank 0) on the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LB selective-scan GB/s (% of HBM peak); LBVim-T images/sec at 1/2/4/8 B200"
+UNIT = "images/s"
+GLOBAL_BATCH_PER_GPU = 256
+CPU_SAMPLE_BATCH = 2
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _workload_config(n, batch, extra=None):
+    c = {"workload": "LBVim-Ti forward, 224^2 patch16, L=197 (middle class token), 24 layers, "
+                     "D=192, E=384, N=16, window M=8, alternating direction",
+         "model": "LBVim-Ti", "global_batch": batch * n, "batch_per_gpu": batch, "seq_len": 197,
+         "parallelism": f"dp{n} (batch-sharded, weights replicated, no collective)",
+         "l2": "flushed between timed steps (256 MiB write, outside the timed events)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (reference CPU path, oracle port)
+
+def _cpu_params(seed=0):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    D, E, N = 192, 384, 16
+    f = np.float32
+    p = {"patch_w": (rng.standard_normal((768, D)) / np.sqrt(768)).astype(f), "patch_b": np.zeros(D, f),
+         "pos": (0.02 * rng.standard_normal((197, D))).astype(f), "cls": (0.02 * rng.standard_normal((1, D))).astype(f)}
+    for i in range(24):
+        dt = np.exp(rng.uniform(np.log(1e-3), np.log(1e-1), E))
+        w = dict(norm_scale=np.ones(D), w_x=rng.standard_normal((D, E)) / np.sqrt(D),
+                 w_z=rng.standard_normal((D, E)) / np.sqrt(D), conv_kernel=rng.uniform(-1, 1, (E, 4)) / 2,
+                 w_b=rng.standard_normal((E, N)) / np.sqrt(E), w_c=rng.standard_normal((E, N)) / np.sqrt(E),
+                 w_delta=rng.standard_normal((E, E)) * 0.1 / np.sqrt(E), delta_bias=dt + np.log(-np.expm1(-dt)),
+                 a_log=np.tile(np.log(np.arange(1, N + 1)), (E, 1)), d_param=np.ones(E),
+                 w_out=rng.standard_normal((E, D)) / np.sqrt(E))
+        for k, v in w.items():
+            p[f"blocks.{i}.{k}"] = v.astype(f)
+    p.update({"head.mlp_w1": (rng.standard_normal((D, 4 * D)) / np.sqrt(D)).astype(f),
+              "head.mlp_b1": np.zeros(4 * D, f),
+              "head.mlp_w2": (rng.standard_normal((4 * D, 1000)) / np.sqrt(4 * D)).astype(f),
+              "head.mlp_b2": np.zeros(1000, f)})
+    return p
+
+
+def cpu_reference_run(steps, warmup, batch=CPU_SAMPLE_BATCH):
+    """Time the reference's CPU path (port) on `batch` images per step."""
+    import numpy as np
+    from oracle import cpu_port
+    cpu_port.build()
+    threads = os.cpu_count() or 1
+    cfg = dict(image_size=224, patch_size=16, in_channels=3, embed_dim=192, inner_dim=384, state_dim=16,
+               depth=24, tile_len=None, class_token="middle")
+    params = _cpu_params()
+    imgs = np.random.default_rng(1).standard_normal((batch, 224, 224, 3)).astype(np.float32)
+    for _ in range(warmup):
+        cpu_port.model_forward(imgs, cfg, params, threads=threads)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        cpu_port.model_forward(imgs, cfg, params, threads=threads)
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    return {"value": batch * steps / total, "unit": UNIT, "cores": threads, "kind": "port",
+            "ms_per_step": total / steps * 1e3,
+            "sample": f"LBVim-Ti fp32 forward on {batch} images per step x {steps} steps (+{warmup} warm-up), "
+                      f"numpy + engine restated in C/OpenMP ({threads} threads; bitwise equal to the "
+                      f"reference numba engine on its verification grid)"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    steps = max(1, min(args.steps, 8))
+    warm = max(1, min(args.warmup, 1))
+    r = cpu_reference_run(steps, warm)
+    line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1) images, random-init weights)",
+            "config": _workload_config(1, CPU_SAMPLE_BATCH, {"note": "bounded CPU sample, scaled to images/s"}),
+            "impl": "reference",
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def scan_alg_bytes(B, L, E, N, s_io, s_bc):
+    """s_in*B*L*(3E + 2N) + s_out*B*L*E + 4*(E*N + 2E)."""
+    return s_io * B * L * 3 * E + s_bc * B * L * 2 * N + s_io * B * L * E + 4 * (E * N + 2 * E)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2506_15976_b200 import model as M
+    from paper_2506_15976_b200 import scan as S
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    B = args.batch
+    cfg = M.lbvim_tiny()
+    params = M.init_params(cfg, seed=0, device=dev)
+    net = M.LBVim(cfg, params, dtype=torch.bfloat16)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    images = torch.randn(B, 224, 224, 3, generator=g, device=dev).to(torch.bfloat16)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    # ---- device-timed steps (inputs resident) -------------------------------
+    run = net.graphed(images)
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        t_wall = time.perf_counter()
+        for s, e in evs:
+            flush.zero_()
+            s.record()
+            run()
+            e.record()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms = sum(s.elapsed_time(e) for s, e in evs)
+    t = torch.tensor([dev_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms = float(t.item())
+    value = world * B * args.steps / (dev_ms / 1e3)
+
+    # ---- end to end through the public API: pinned host in, logits out ------
+    host_imgs = [images.cpu().pin_memory() for _ in range(2)]
+    runs = [run, net.graphed(images)]
+    outs = [torch.empty((B, cfg.num_classes), dtype=torch.float32).pin_memory() for _ in range(2)]
+    copy = torch.cuda.Stream(device=dev)
+    comp = torch.cuda.current_stream()
+    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    comp_done = [torch.cuda.Event() for _ in range(2)]
+    e2e_steps = args.steps
+
+    def e2e_loop(n):
+        with torch.cuda.stream(copy):
+            runs[0].static_in.copy_(host_imgs[0], non_blocking=True)
+            h2d_done[0].record(copy)
+        for i in range(n):
+            k = i % 2
+            comp.wait_event(h2d_done[k])
+            runs[k].graph.replay()
+            comp_done[k].record(comp)
+            with torch.cuda.stream(copy):
+                if i + 1 < n:
+                    kn = (i + 1) % 2
+                    if i >= 1:
+                        copy.wait_event(comp_done[kn])
+                    runs[kn].static_in.copy_(host_imgs[kn], non_blocking=True)
+                    h2d_done[kn].record(copy)
+                copy.wait_event(comp_done[k])
+                outs[k].copy_(runs[k].static_out, non_blocking=True)
+        torch.cuda.synchronize()
+
+    e2e_loop(2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_loop(e2e_steps)
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * e2e_steps / float(t.item())
+    h2d_bytes = host_imgs[0].numel() * host_imgs[0].element_size()
+    d2h_bytes = outs[0].numel() * outs[0].element_size()
+
+    # ---- roofline: the fused scan kernel, timed live per launch -------------
+    scan_evs = []
+    orig = S.lbm_selective_scan_fwd
+
+    def timed_scan(*a, **kw):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        r = orig(*a, **kw)
+        e.record()
+        scan_evs.append((s, e))
+        return r
+
+    M.lbm_selective_scan_fwd = timed_scan
+    try:
+        for _ in range(2):
+            net.forward(images)
+        torch.cuda.synchronize()
+        scan_evs.clear()
+        for _ in range(max(2, args.steps // 2)):
+            flush.zero_()
+            net.forward(images)
+        torch.cuda.synchronize()
+    finally:
+        M.lbm_selective_scan_fwd = orig
+    scan_ms = sum(s.elapsed_time(e) for s, e in scan_evs) / len(scan_evs)
+    E, N, L = cfg.inner_dim, cfg.state_dim, cfg.seq_len
+    nbytes = scan_alg_bytes(B, L, E, N, 2, 2)
+    achieved = nbytes / (scan_ms / 1e3) / 1e9
+    peaks = _peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback 6650 GB/s (B200_PROFILING.md)"
+    peak = peak or 6650.0
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tr.get("lbvim_t_scan_bytes_per_launch")
+    except Exception:
+        pass
+    step_ms = dev_ms / args.steps
+    scan_share = cfg.depth * scan_ms / step_ms
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_run(steps=2, warmup=1)
+        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (N(0,1) images, random-init weights of the reference architecture)",
+            "config": _workload_config(world, B),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": d2h_bytes,
+                    "note": "graph replay per step; pinned host images H2D and logits D2H every step on a "
+                            "copy stream, double-buffered"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "lbs::fwd_kernel (fused discretize + LB scan + D skip + SiLU gate)",
+                         "bytes_per_launch": nbytes, "ms_per_launch": scan_ms, "peak_source": peak_src,
+                         "share_of_step": scan_share,
+                         "note": "MUFU/issue-bound: 1 ex2 + ~3.5 packed FP32 ops per state-step (DESIGN.md)"},
+            "cpu_baseline": cpu,
+            "gpu_launches": 2 * cfg.depth * args.steps,
+            "clocks": clk.summary(),
+            "wall_s_timed_region": t_wall,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=GLOBAL_BATCH_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

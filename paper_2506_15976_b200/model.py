@@ -1,0 +1,291 @@
+"""LBVim backbone on the B200 path — the caller of the fused LB scan.
+
+Mirrors the reference model (model.py:25-325) and block (block.py:141-190):
+
+    patchify -> linear -> [class token] -> +pos -> U x block -> head
+    block: RMSNorm -> x = xn W_x, z = xn W_z -> causal conv1d + SiLU ->
+           [delta | B | C] = xs [W_delta | W_b | W_c] -> LB scan (+D skip,
+           x SiLU(z) gate) -> out = yg W_out + residual -> (sequence reversal)
+
+B200 design:
+  * the per-block sequence reversal (block.py:180-181, model.py:216-218) is
+    never materialised: tokens stay in input order and block i runs its conv
+    and scan in direction (-1)^i by flip-on-load (LBS_FLAG_REVERSE), which is
+    exactly equivalent;
+  * W_delta, W_b, W_c are one fused GEMM; delta, B and C are strided column
+    views of its output, and z is a strided view of the in-projection output,
+    passed straight to the scan kernel (no copies);
+  * GEMMs stay on stock torch/cuBLAS (north star); conv+SiLU and the scan
+    are the hand-written sm_100a kernels;
+  * the whole forward can be captured in one CUDA graph (``LBVim.graphed``).
+
+Weights follow the reference's shapes and initialisation (block.py:52-73,
+model.py:118-148) including the full-rank E x E delta projection.  The
+reference's conv tap order is kept: kernel[e, q] multiplies x[l - q].
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+import torch.nn.functional as F
+
+from .conv import causal_conv1d_silu_fwd
+from .errors import ShapeError
+from .scan import lbm_selective_scan_fwd
+from .tiling import select_tile_len
+
+RMS_EPS = 1e-6  # nn.py:13
+CLASS_TOKENS = {"none": 0, "head": 1, "middle": 1, "double": 2}  # model.py:22
+
+
+@dataclass
+class ModelConfig:
+    """model.py:25-115 (same fields and defaults)."""
+
+    image_size: int = 32
+    patch_size: int = 4
+    in_channels: int = 1
+    embed_dim: int = 64
+    inner_dim: int = 128
+    state_dim: int = 16
+    depth: int = 4
+    tile_len: int | None = None
+    head: str = "gap"
+    map_heads: int = 4
+    class_token: str = "none"
+    num_classes: int = 2
+    conv_width: int = 4
+    reverse_between_blocks: bool = True
+    unreverse_output: bool = True
+    discretize_mode: str = "exp"
+    scan_variant: str = "lbm"
+
+    def __post_init__(self):
+        if self.image_size % self.patch_size:
+            raise ShapeError(f"image size {self.image_size} not divisible by patch size {self.patch_size}")
+        if self.depth < 1:
+            raise ShapeError("depth must be >= 1")
+        if self.head not in ("gap", "map"):
+            raise ShapeError(f"unknown head {self.head!r}")
+        if self.class_token not in CLASS_TOKENS:
+            raise ShapeError(f"unknown class token mode {self.class_token!r}")
+        if self.scan_variant not in ("forward", "lbm"):
+            raise ShapeError(f"unsupported scan variant {self.scan_variant!r}")
+
+    @property
+    def num_patches(self) -> int:
+        return (self.image_size // self.patch_size) ** 2
+
+    @property
+    def seq_len(self) -> int:
+        return self.num_patches + CLASS_TOKENS[self.class_token]
+
+    @property
+    def resolved_tile_len(self) -> int:
+        return select_tile_len(self.seq_len) if self.tile_len in (None, "auto") else int(self.tile_len)
+
+
+def lbvim_tiny(**kw) -> ModelConfig:
+    """LBVim-Ti at 224^2, patch 16 (BASELINE configs[1]): D=192, E=384, N=16,
+    24 layers, L = 196 patches + 1 middle class token = 197."""
+    base = dict(image_size=224, patch_size=16, in_channels=3, embed_dim=192, inner_dim=384,
+                state_dim=16, depth=24, head="gap", class_token="middle", num_classes=1000)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
+def lbvim_small(**kw) -> ModelConfig:
+    """LBVim-S: D=384, E=768 (BASELINE configs[2], [3])."""
+    base = dict(image_size=224, patch_size=16, in_channels=3, embed_dim=384, inner_dim=768,
+                state_dim=16, depth=24, head="gap", class_token="middle", num_classes=1000)
+    base.update(kw)
+    return ModelConfig(**base)
+
+
+BLOCK_FIELDS = ("norm_scale", "w_x", "w_z", "conv_kernel", "w_b", "w_c",
+                "w_delta", "delta_bias", "a_log", "d_param", "w_out")
+
+
+def init_params(cfg: ModelConfig, seed: int = 0, device="cuda", dtype=torch.float32) -> dict:
+    """Random init with the reference's distributions (block.py:52-73,
+    model.py:118-148), drawn from a seeded torch generator on the device."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    D, E, N, k = cfg.embed_dim, cfg.inner_dim, cfg.state_dim, cfg.conv_width
+    patch_in = cfg.patch_size ** 2 * cfg.in_channels
+
+    def randn(*s, scale=1.0):
+        return torch.randn(*s, generator=g, device=device, dtype=torch.float32) * scale
+
+    def unif(lo, hi, *s):
+        return torch.empty(*s, device=device, dtype=torch.float32).uniform_(lo, hi, generator=g)
+
+    p = {
+        "patch_w": randn(patch_in, D, scale=1 / math.sqrt(patch_in)),
+        "patch_b": torch.zeros(D, device=device),
+        "pos": randn(cfg.seq_len, D, scale=0.02),
+    }
+    if CLASS_TOKENS[cfg.class_token]:
+        p["cls"] = randn(CLASS_TOKENS[cfg.class_token], D, scale=0.02)
+    for i in range(cfg.depth):
+        dt = torch.exp(unif(math.log(1e-3), math.log(1e-1), E))
+        blk = {
+            "norm_scale": torch.ones(D, device=device),
+            "w_x": randn(D, E, scale=1 / math.sqrt(D)),
+            "w_z": randn(D, E, scale=1 / math.sqrt(D)),
+            "conv_kernel": unif(-1, 1, E, k) / math.sqrt(k),
+            "w_b": randn(E, N, scale=1 / math.sqrt(E)),
+            "w_c": randn(E, N, scale=1 / math.sqrt(E)),
+            "w_delta": randn(E, E, scale=0.1 / math.sqrt(E)),
+            "delta_bias": dt + torch.log(-torch.expm1(-dt)),
+            "a_log": torch.log(torch.arange(1, N + 1, device=device, dtype=torch.float32)).repeat(E, 1),
+            "d_param": torch.ones(E, device=device),
+            "w_out": randn(E, D, scale=1 / math.sqrt(E)),
+        }
+        for f, v in blk.items():
+            p[f"blocks.{i}.{f}"] = v
+    if cfg.head == "map":
+        p["head.q"] = randn(D, scale=1 / math.sqrt(D))
+        p["head.wk"] = randn(D, D, scale=1 / math.sqrt(D))
+        p["head.wv"] = randn(D, D, scale=1 / math.sqrt(D))
+    hidden = 4 * D
+    p["head.mlp_w1"] = randn(D, hidden, scale=1 / math.sqrt(D))
+    p["head.mlp_b1"] = torch.zeros(hidden, device=device)
+    p["head.mlp_w2"] = randn(hidden, cfg.num_classes, scale=1 / math.sqrt(hidden))
+    p["head.mlp_b2"] = torch.zeros(cfg.num_classes, device=device)
+    return {k: v.to(dtype) for k, v in p.items()}
+
+
+class LBVim:
+    """Inference-time LBVim on the fused kernels.  ``dtype`` is the activation
+    / weight dtype (bf16 for throughput, fp32 for parity); scan state is fp32."""
+
+    def __init__(self, cfg: ModelConfig, params: dict, dtype=torch.bfloat16):
+        self.cfg = cfg
+        self.dtype = dtype
+        D, E, N = cfg.embed_dim, cfg.inner_dim, cfg.state_dim
+        self.M = cfg.resolved_tile_len
+        cast = lambda t: t.to(dtype).contiguous()
+        f32 = lambda t: t.to(torch.float32).contiguous()
+        self.patch_w, self.patch_b = cast(params["patch_w"]), cast(params["patch_b"])
+        self.pos = cast(params["pos"])
+        self.cls = cast(params["cls"]) if "cls" in params else None
+        self.blocks = []
+        for i in range(cfg.depth):
+            w = {f: params[f"blocks.{i}.{f}"] for f in BLOCK_FIELDS}
+            self.blocks.append(dict(
+                norm_scale=cast(w["norm_scale"]),
+                w_in=cast(torch.cat([w["w_x"], w["w_z"]], dim=1)),                  # (D, 2E)
+                conv_kernel=f32(w["conv_kernel"]),                                    # (E, k)
+                w_xp=cast(torch.cat([w["w_delta"], w["w_b"], w["w_c"]], dim=1)),      # (E, E+2N)
+                A=f32(-torch.exp(w["a_log"].float())),
+                D=f32(w["d_param"]), delta_bias=f32(w["delta_bias"]),
+                w_out=cast(w["w_out"]),
+            ))
+        self.head = {k: cast(v) for k, v in params.items() if k.startswith("head.")}
+        self._graph = None
+
+    # -- pieces -----------------------------------------------------------------
+    def patch_embed(self, images):
+        """model.py:190-201; images (B, H, W, C) channel-last like the reference."""
+        cfg = self.cfg
+        B, H, W, C = images.shape
+        if H != cfg.image_size or W != cfg.image_size or C != cfg.in_channels:
+            raise ShapeError(f"image shape {tuple(images.shape[1:])} does not match config")
+        p, g = cfg.patch_size, cfg.image_size // cfg.patch_size
+        x = images.to(self.dtype).reshape(B, g, p, g, p, C).permute(0, 1, 3, 2, 4, 5).reshape(B, g * g, p * p * C)
+        tok = torch.addmm(self.patch_b, x.reshape(-1, x.shape[-1]), self.patch_w).reshape(B, g * g, -1)
+        ct = cfg.class_token
+        if ct != "none":
+            cls = self.cls
+            D = tok.shape[-1]
+            if ct == "head":
+                tok = torch.cat([cls[0].expand(B, 1, D), tok], 1)
+            elif ct == "middle":
+                mid = tok.shape[1] // 2
+                tok = torch.cat([tok[:, :mid], cls[0].expand(B, 1, D), tok[:, mid:]], 1)
+            else:
+                tok = torch.cat([cls[0].expand(B, 1, D), tok, cls[1].expand(B, 1, D)], 1)
+        return (tok + self.pos).contiguous()
+
+    def block(self, T, w, reverse: bool):
+        """block.py:158-190 with the output reversal replaced by direction."""
+        B, L, D = T.shape
+        E, N = w["A"].shape
+        xn = F.rms_norm(T, (D,), w["norm_scale"], eps=RMS_EPS)
+        xz = (xn.reshape(-1, D) @ w["w_in"]).reshape(B, L, 2 * E)
+        x, z = xz[..., :E], xz[..., E:]
+        xs = causal_conv1d_silu_fwd(x, w["conv_kernel"], reverse=reverse)
+        proj = (xs.reshape(-1, E) @ w["w_xp"]).reshape(B, L, E + 2 * N)
+        yg = lbm_selective_scan_fwd(
+            xs, proj[..., :E], w["A"], proj[..., E:E + N], proj[..., E + N:], D=w["D"], z=z,
+            delta_bias=w["delta_bias"], window=self.M, reverse=reverse,
+            lb=self.cfg.scan_variant == "lbm", discretize_mode=self.cfg.discretize_mode)
+        return torch.addmm(T.reshape(-1, D), yg.reshape(-1, E), w["w_out"]).reshape(B, L, D)
+
+    def run_blocks(self, tok):
+        """model.py:204-222.  Returns tokens in original order; the number of
+        reference reversals applied is tracked only for the head's index map."""
+        rev = self.cfg.reverse_between_blocks
+        for i, w in enumerate(self.blocks):
+            tok = self.block(tok, w, reverse=rev and (i % 2 == 1))
+        return tok
+
+    def head_forward(self, tok):
+        """model.py:238-325 heads.  Tokens arrive in original order here.  The
+        reference reads class tokens at p or L-1-p depending on how many
+        reversals are left (model.py:225-229,307-312) — both are original
+        position p — and its GAP / MAP pools are order-invariant."""
+        cfg = self.cfg
+        ct = cfg.class_token
+        if ct != "none":
+            pos = {"head": [0], "middle": [cfg.num_patches // 2], "double": [0, cfg.seq_len - 1]}[ct]
+            pooled = tok[:, pos].float().mean(1)
+        elif cfg.head == "gap":
+            pooled = tok.float().mean(1)
+        else:
+            B, L, D = tok.shape
+            nh = cfg.map_heads
+            dh = D // nh
+            t = tok.float()
+            K = (t @ self.head["head.wk"].float()).reshape(B, L, nh, dh)
+            V = (t @ self.head["head.wv"].float()).reshape(B, L, nh, dh)
+            q = self.head["head.q"].float().reshape(nh, dh)
+            att = torch.softmax(torch.einsum("blhd,hd->blh", K, q) / math.sqrt(dh), dim=1)
+            pooled = torch.einsum("blh,blhd->bhd", att, V).reshape(B, D)
+        h1 = F.gelu(pooled @ self.head["head.mlp_w1"].float() + self.head["head.mlp_b1"].float(),
+                    approximate="tanh")
+        return h1 @ self.head["head.mlp_w2"].float() + self.head["head.mlp_b2"].float()
+
+    @torch.no_grad()
+    def forward(self, images):
+        return self.head_forward(self.run_blocks(self.patch_embed(images)))
+
+    __call__ = forward
+
+    # -- CUDA graph ---------------------------------------------------------------
+    @torch.no_grad()
+    def graphed(self, example_images):
+        """Capture forward() for a fixed input shape; returns a callable that
+        copies new images into the static input and replays the graph."""
+        static_in = example_images.clone()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(2):
+                self.forward(static_in)
+        torch.cuda.current_stream().wait_stream(s)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            static_out = self.forward(static_in)
+
+        def run(images=None):
+            if images is not None:
+                static_in.copy_(images, non_blocking=True)
+            graph.replay()
+            return static_out
+
+        run.graph, run.static_in, run.static_out = graph, static_in, static_out
+        return run

@@ -1,0 +1,95 @@
+"""LBVim block/model on the fused kernels vs the reference's own outputs
+(golden vectors) and the oracle.  -m gpu."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import lbscan_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2506_15976_b200.model import BLOCK_FIELDS, LBVim, ModelConfig, init_params  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _model_from_golden(i):
+    g = np.load(os.path.join(GOLD, "model.npz"))
+    pre = f"m{i}_"
+    cfg = {k[len(pre) + 4:]: g[k].item() for k in g.files if k.startswith(pre + "cfg_")}
+    cfg["tile_len"] = None if cfg["tile_len"] in (None, "auto") else int(cfg["tile_len"])
+    for k in ("reverse_between_blocks", "unreverse_output"):
+        cfg[k] = bool(cfg[k])
+    for k in ("image_size", "patch_size", "in_channels", "embed_dim", "inner_dim", "state_dim", "depth",
+              "map_heads", "num_classes", "conv_width"):
+        cfg[k] = int(cfg[k])
+    params = {k[len(pre) + 2:]: torch.tensor(g[k], dtype=torch.float32, device="cuda")
+              for k in g.files if k.startswith(pre + "p_")}
+    return ModelConfig(**cfg), params, g[pre + "images"], g[pre + "logits"]
+
+
+@pytest.mark.parametrize("i", range(3))
+def test_model_forward_matches_reference_golden(i):
+    cfg, params, images, ref = _model_from_golden(i)
+    m = LBVim(cfg, params, dtype=torch.float32)
+    got = m(torch.tensor(images, dtype=torch.float32, device="cuda")).cpu().numpy()
+    assert O.max_rel_err(got, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_block_matches_reference_golden(i):
+    g = np.load(os.path.join(GOLD, "block.npz"))
+    D, E, N, L, B, M, k, linear, rev, seed = [int(v) for v in g[f"b{i}_meta"]]
+    cfg = ModelConfig(image_size=4, patch_size=4, embed_dim=D, inner_dim=E, state_dim=N, depth=1,
+                      tile_len=M, conv_width=k, discretize_mode="linear" if linear else "exp")
+    params = {f"blocks.0.{f}": torch.tensor(g[f"b{i}_w_{f}"], dtype=torch.float32, device="cuda")
+              for f in BLOCK_FIELDS}
+    params.update(patch_w=torch.zeros(16, D), patch_b=torch.zeros(D), pos=torch.zeros(1, D))
+    m = LBVim(cfg, {k: v.cuda() for k, v in params.items()}, dtype=torch.float32)
+    T = torch.tensor(g[f"b{i}_T"], dtype=torch.float32, device="cuda")
+    out = m.block(T, m.blocks[0], reverse=False).cpu().numpy()
+    ref = g[f"b{i}_out"]
+    ref = ref[:, ::-1] if rev else ref  # the reference reverses the block output
+    assert O.max_rel_err(out, ref) <= 1e-5
+    # flip-on-load: a reverse-direction block on the reversed sequence equals
+    # the reversed forward-direction block
+    Tr = torch.flip(T, dims=[1])
+    out_r = m.block(Tr, m.blocks[0], reverse=True).cpu().numpy()
+    assert O.max_rel_err(out_r[:, ::-1], ref) <= 1e-5
+
+
+def test_lbvim_tiny_bf16_vs_fp32_and_graph():
+    """Full-size LBVim-Ti (24 layers, L=197) at a small batch: bf16 path vs the
+    fp32 path of the same weights, and the CUDA-graph replay is identical."""
+    from paper_2506_15976_b200.model import lbvim_tiny
+    cfg = lbvim_tiny()
+    params = init_params(cfg, seed=0)
+    imgs = torch.randn(4, 224, 224, 3, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+    m32 = LBVim(cfg, params, dtype=torch.float32)
+    m16 = LBVim(cfg, params, dtype=torch.bfloat16)
+    l32 = m32(imgs)
+    l16 = m16(imgs)
+    assert torch.isfinite(l16).all()
+    rel = (l16 - l32).abs().max() / l32.abs().max()
+    assert rel.item() <= 5e-2
+    run = m16.graphed(imgs)
+    torch.testing.assert_close(run(imgs), l16, rtol=0, atol=0)
+
+
+def test_lbvim_tiny_fp32_vs_oracle_subsample():
+    """LBVim-Ti structure (24 layers) with the CPU oracle on one image, fp32."""
+    from paper_2506_15976_b200.model import lbvim_tiny
+    cfg = lbvim_tiny(depth=4)
+    params = init_params(cfg, seed=3)
+    imgs = torch.randn(1, 224, 224, 3, device="cuda", generator=torch.Generator(device="cuda").manual_seed(2))
+    got = LBVim(cfg, params, dtype=torch.float32)(imgs).cpu().numpy()
+    npp = {k: v.double().cpu().numpy() for k, v in params.items()}
+    ocfg = dict(image_size=224, patch_size=16, in_channels=3, embed_dim=192, inner_dim=384, state_dim=16,
+                depth=4, tile_len=None, head="gap", class_token="middle")
+    ref = O.model_forward(imgs.double().cpu().numpy(), ocfg, npp)
+    assert O.max_rel_err(got, ref) <= 1e-4
