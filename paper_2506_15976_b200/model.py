@@ -242,7 +242,7 @@ class LBVim:
         ct = cfg.class_token
         if ct != "none":
             pos = {"head": [0], "middle": [cfg.num_patches // 2], "double": [0, cfg.seq_len - 1]}[ct]
-            pooled = tok[:, pos].float().mean(1)
+            pooled = torch.stack([tok[:, q] for q in pos], 1).float().mean(1)  # graph-capturable
         elif cfg.head == "gap":
             pooled = tok.float().mean(1)
         else:
