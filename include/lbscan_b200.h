@@ -26,6 +26,7 @@
  *   lbs_causal_conv1d_silu_fwd/bwd <- nn.causal_conv1d + nn.silu (nn.py:87-99,25-26) and
  *                              nn.causal_conv1d_grad + silu_grad (nn.py:102-114,29-31).
  *   lbs_select_tile_len     <- engine.select_tile_len (engine.py:54-62).
+ *   lbs_rms_norm_fwd        <- nn.rms_norm (nn.py:55-58), the block's first op (block.py:170).
  *
  * Layout: sequence tensors are addressed as element (b, l, e) at
  *   base + b*stride[0] + l*stride[1] + e*stride[2]      (reference: channel-last (B,L,E))
@@ -125,6 +126,17 @@ typedef struct lbs_conv_args {
 } lbs_conv_args;
 #define LBS_CONV_SILU (1u << 4)
 
+/* RMSNorm with learned scale (nn.rms_norm, nn.py:55-58): out = x / sqrt(mean(x^2) + eps) * scale,
+ * over rows of `dim` contiguous elements.  dim % (16/sizeof(elem)) == 0, rows 16-byte aligned. */
+typedef struct lbs_norm_args {
+  int64_t rows, dim;
+  int32_t io_dtype;
+  float eps;
+  const void* x;   int64_t x_row_stride;
+  const float* scale;       /* (dim) fp32 */
+  void* out;       int64_t out_row_stride;
+} lbs_norm_args;
+
 int lbs_abi_version(void);
 const char* lbs_last_error(void);
 int64_t lbs_select_tile_len(int64_t seqlen);
@@ -138,6 +150,8 @@ int lbs_scan_bwd(const lbs_scan_bwd_args* args, void* workspace, size_t workspac
                  void* cuda_stream);
 
 int lbs_prediscretized_fwd(const lbs_prediscretized_args* args, void* cuda_stream);
+
+int lbs_rms_norm_fwd(const lbs_norm_args* args, void* cuda_stream);
 
 size_t lbs_causal_conv1d_bwd_workspace_bytes(const lbs_conv_args* args);
 int lbs_causal_conv1d_fwd(const lbs_conv_args* args, void* cuda_stream);

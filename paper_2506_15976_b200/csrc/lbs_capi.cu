@@ -199,6 +199,16 @@ int lbs_prediscretized_fwd(const lbs_prediscretized_args* a, void* stream) {
                      "lbs_prediscretized_fwd");
 }
 
+int lbs_rms_norm_fwd(const lbs_norm_args* a, void* stream) {
+  if (!a) return fail(LBS_ERR_INVALID, "null args");
+  if (a->rows < 1 || a->dim < 1) return fail(LBS_ERR_INVALID, "rows and dim must be >= 1");
+  if (a->io_dtype != LBS_F32 && a->io_dtype != LBS_BF16) return fail(LBS_ERR_INVALID, "dtype must be f32 or bf16");
+  if (!a->x || !a->scale || !a->out) return fail(LBS_ERR_INVALID, "null tensor");
+  if (a->rows > (int64_t)1 << 34) return fail(LBS_ERR_UNSUPPORTED, "too many rows");
+  lbs::NormParams p{a->rows, (int)a->dim, a->eps, a->x, a->x_row_stride, a->scale, a->out, a->out_row_stride};
+  return cuda_status(lbs::launch_rms_norm(p, a->io_dtype, (cudaStream_t)stream), "lbs_rms_norm_fwd");
+}
+
 size_t lbs_scan_bwd_workspace_bytes(const lbs_scan_bwd_args* a) {
   (void)a;
   return 0;

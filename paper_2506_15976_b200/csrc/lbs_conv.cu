@@ -61,14 +61,26 @@ __global__ void __launch_bounds__(kConvThreads) conv_fwd_kernel(ConvParams p) {
     const int l = l0 - q;
     hist[q] = (q < p.K && l >= 0) ? ld<T>(xp + phys(l) * p.x.s1) : 0.f;
   }
-  for (int l = l0; l < l1; ++l) {
-    hist[0] = ld<T>(xp + phys(l) * p.x.s1);
-    float acc = bias;
+  // groups of 8 steps: all 8 loads are issued before any use (memory-level
+  // parallelism), then the window slides through them in registers
+  const long long xs = rev ? -p.x.s1 : p.x.s1;
+  const long long os = rev ? -p.so1 : p.so1;
+  const T* xl = xp + phys(l0) * p.x.s1;
+  T* ol = op + phys(l0) * p.so1;
+  for (int l = l0; l < l1; l += 8) {
+    float xv[8];
 #pragma unroll
-    for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], hist[q], acc);
-    st<T>(op + phys(l) * p.so1, act ? silu_f(acc) : acc);
+    for (int i = 0; i < 8; ++i) xv[i] = (l + i < l1) ? ld<T>(xl + (long long)(l - l0 + i) * xs) : 0.f;
 #pragma unroll
-    for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
+    for (int i = 0; i < 8; ++i) {
+      hist[0] = xv[i];
+      float acc = bias;
+#pragma unroll
+      for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], hist[q], acc);
+      if (l + i < l1) st<T>(ol + (long long)(l - l0 + i) * os, act ? silu_f(acc) : acc);
+#pragma unroll
+      for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
+    }
   }
 }
 

@@ -47,4 +47,16 @@ struct PreParams {
 };
 cudaError_t launch_prediscretized(const PreParams& p, bool f64, cudaStream_t st);
 
+struct NormParams {
+  long long rows;
+  int D;
+  float eps;
+  const void* x;
+  long long sx;
+  const float* scale;
+  void* out;
+  long long so;
+};
+cudaError_t launch_rms_norm(const NormParams& p, int dtype, cudaStream_t st);
+
 }  // namespace lbs

@@ -1,0 +1,100 @@
+// RMSNorm with learned scale (nn.rms_norm, nn.py:55-58; eps 1e-6, no bias) —
+// the first op of every LBVim block (block.py:170).  HBM-bound: one warp per
+// token row, 16-byte vector loads/stores, fp32 accumulation.
+#include "lbs_common.cuh"
+#include "lbs_internal.h"
+
+namespace lbs {
+
+template <typename T, int VPL>  // VPL = 16-byte vectors per lane (row <= 32*VPL*EPV)
+__global__ void __launch_bounds__(256) rms_norm_kernel(const T* __restrict__ x, const float* __restrict__ scale,
+                                                       T* __restrict__ out, long long rows, int D, float eps,
+                                                       long long sx, long long so) {
+  constexpr int EPV = 16 / sizeof(T);
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const T* xr = x + row * sx;
+  T* orow = out + row * so;
+  float v[VPL][EPV];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c0 = (lane + 32 * k) * EPV;
+    if (c0 < D) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(xr + c0);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < EPV; ++i) {
+        v[k][i] = to_f(e[i]);
+        ss = fmaf(v[k][i], v[k][i], ss);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = rsqrtf(ss / (float)D + eps);
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c0 = (lane + 32 * k) * EPV;
+    if (c0 < D) {
+      uint4 raw;
+      T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < EPV; ++i) {
+        float y = v[k][i] * inv * scale[c0 + i];
+        if constexpr (sizeof(T) == 4) e[i] = y;
+        else e[i] = __float2bfloat16_rn(y);
+      }
+      *reinterpret_cast<uint4*>(orow + c0) = raw;
+    }
+  }
+}
+
+// any D / alignment: one warp per row, scalar strided accesses
+template <typename T>
+__global__ void __launch_bounds__(256) rms_norm_scalar_kernel(const T* __restrict__ x, const float* __restrict__ scale,
+                                                              T* __restrict__ out, long long rows, int D, float eps,
+                                                              long long sx, long long so) {
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  float ss = 0.f;
+  for (int c = lane; c < D; c += 32) {
+    const float v = to_f(x[row * sx + c]);
+    ss = fmaf(v, v, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = rsqrtf(ss / (float)D + eps);
+  for (int c = lane; c < D; c += 32) st<T>(out + row * so + c, to_f(x[row * sx + c]) * inv * scale[c]);
+}
+
+template <typename T>
+static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
+  constexpr int EPV = 16 / sizeof(T);
+  const int vpl = (p.D + 32 * EPV - 1) / (32 * EPV);
+  dim3 block(256), grid((unsigned)((p.rows + 7) / 8));
+  const T* x = static_cast<const T*>(p.x);
+  T* o = static_cast<T*>(p.out);
+  const bool vec = p.D % EPV == 0 && (p.sx * (long long)sizeof(T)) % 16 == 0 &&
+                   (p.so * (long long)sizeof(T)) % 16 == 0 && reinterpret_cast<uintptr_t>(p.x) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(p.out) % 16 == 0 && vpl <= 4;
+  if (!vec) {
+    rms_norm_scalar_kernel<T><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+    return cudaGetLastError();
+  }
+  if (vpl <= 1) rms_norm_kernel<T, 1><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+  else if (vpl <= 2) rms_norm_kernel<T, 2><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+  else if (vpl <= 4) rms_norm_kernel<T, 4><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+  else return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rms_norm(const NormParams& p, int dtype, cudaStream_t st) {
+  if (dtype == LBS_F32) return launch_norm_t<float>(p, st);
+  if (dtype == LBS_BF16) return launch_norm_t<__nv_bfloat16>(p, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lbs

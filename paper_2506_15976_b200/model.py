@@ -34,6 +34,7 @@ import torch.nn.functional as F
 
 from .conv import causal_conv1d_silu_fwd
 from .errors import ShapeError
+from .norm import rms_norm
 from .scan import lbm_selective_scan_fwd
 from .tiling import select_tile_len
 
@@ -176,7 +177,7 @@ class LBVim:
         for i in range(cfg.depth):
             w = {f: params[f"blocks.{i}.{f}"] for f in BLOCK_FIELDS}
             self.blocks.append(dict(
-                norm_scale=cast(w["norm_scale"]),
+                norm_scale=cast(w["norm_scale"]), norm_f32=f32(w["norm_scale"]),
                 w_in=cast(torch.cat([w["w_x"], w["w_z"]], dim=1)),                  # (D, 2E)
                 conv_kernel=f32(w["conv_kernel"]),                                    # (E, k)
                 w_xp=cast(torch.cat([w["w_delta"], w["w_b"], w["w_c"]], dim=1)),      # (E, E+2N)
@@ -214,7 +215,7 @@ class LBVim:
         """block.py:158-190 with the output reversal replaced by direction."""
         B, L, D = T.shape
         E, N = w["A"].shape
-        xn = F.rms_norm(T, (D,), w["norm_scale"], eps=RMS_EPS)
+        xn = rms_norm(T, w["norm_f32"], eps=RMS_EPS)
         xz = (xn.reshape(-1, D) @ w["w_in"]).reshape(B, L, 2 * E)
         x, z = xz[..., :E], xz[..., E:]
         xs = causal_conv1d_silu_fwd(x, w["conv_kernel"], reverse=reverse)

@@ -246,3 +246,16 @@ def test_conv_golden():
     dx, dw, _ = causal_conv1d_silu_bwd(dev(g["x"]), dev(g["k"]), None, dev(g["g"]), silu=False)
     assert O.max_rel_err(dx.cpu().numpy(), g["gx"]) <= TOL_F32
     assert O.max_rel_err(dw.cpu().numpy(), g["gk"]) <= TOL_F32
+
+
+@pytest.mark.parametrize("dtype,D", [(torch.float32, 192), (torch.bfloat16, 192), (torch.bfloat16, 384),
+                                     (torch.float32, 8)])
+def test_rms_norm(dtype, D):
+    from paper_2506_15976_b200.norm import rms_norm
+    rng = O.seeded_rng(D)
+    x = rng.standard_normal((3, 37, D))
+    s = rng.uniform(0.5, 1.5, D)
+    got = rms_norm(dev(x, dtype), dev(s)).float().cpu().numpy()
+    xq = dev(x, dtype).double().cpu().numpy()
+    ref = O.rms_norm(xq, s)
+    assert O.max_rel_err(got, ref) <= (TOL_F32 if dtype == torch.float32 else 1e-2)
