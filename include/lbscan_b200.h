@@ -74,15 +74,23 @@ typedef struct lbs_scan_fwd_args {
   const void* z;      int64_t z_stride[3];    /* or NULL: no gate     */
   void* out;          int64_t out_stride[3];
   float* last_state;                          /* (B, E, N) or NULL    */
-  float* checkpoints;  /* NULL, or (B, ceil(L/ckpt_len), E, N): state entering each chunk */
-  int64_t ckpt_len;    /* multiple of window when checkpoints != NULL                       */
+  /* Training checkpoints for lbs_scan_bwd: NULL, or lbs_scan_ckpt_bytes() of fp32
+   * (opaque layout: the state entering every backward chunk).  ckpt_len must equal
+   * lbs_scan_ckpt_len(seqlen, window).  With checkpoints != NULL, out may be NULL
+   * (checkpoint-only sweep).                                                       */
+  float* checkpoints;
+  int64_t ckpt_len;
 } lbs_scan_fwd_args;
 
-/* Fused LB selective scan, backward.  Inputs as in the forward plus dout; the
- * forward's checkpoints (or NULL: recomputed internally in the workspace).
- * Outputs (fp32 unless noted): du, ddelta, dz in io dtype (dz NULL iff z NULL);
- * dA (E,N), dD (E), ddelta_bias (E) — accumulated (+=) into caller-zeroed fp32;
- * dB, dC (b,l,n) in fp32, written (not accumulated).                                    */
+/* Fused LB selective scan, backward (autodiff.lbm_scan_grad chained through
+ * block._discretize_backward and the gate).  Inputs as in the forward plus dout;
+ * fwd.checkpoints from the training forward (or NULL: a checkpoint-only forward
+ * sweep runs first, into the workspace).  fwd.out / fwd.last_state are ignored.
+ * Outputs: du, ddelta, dz in the io dtype (dz given iff z is), flip-on-store for
+ * LBS_FLAG_REVERSE; dA (E,N), dD (E), ddelta_bias (E) fp32, ACCUMULATED (+=) so
+ * several calls can share one gradient buffer (dD / ddelta_bias may be NULL);
+ * dB, dC (b,l,n) fp32, written.  Deterministic: all reductions are fixed-order
+ * partial sums (no atomics).                                                       */
 typedef struct lbs_scan_bwd_args {
   lbs_scan_fwd_args fwd;   /* fwd.out / fwd.last_state are ignored */
   const void* dout;   int64_t dout_stride[3];
@@ -140,6 +148,11 @@ typedef struct lbs_norm_args {
 int lbs_abi_version(void);
 const char* lbs_last_error(void);
 int64_t lbs_select_tile_len(int64_t seqlen);
+
+/* Steps between training checkpoints (= the backward's chunk) for a window, and the
+ * checkpoint buffer size for a forward call; -1 / 0 when the window is unsupported. */
+int64_t lbs_scan_ckpt_len(int64_t seqlen, int64_t window);
+size_t lbs_scan_ckpt_bytes(const lbs_scan_fwd_args* args);
 
 size_t lbs_scan_fwd_workspace_bytes(const lbs_scan_fwd_args* args);
 int lbs_scan_fwd(const lbs_scan_fwd_args* args, void* workspace, size_t workspace_bytes,

@@ -90,6 +90,7 @@ class NormArgs(C.Structure):
 # every symbol include/lbscan_b200.h declares (tests check the export table)
 EXPORTS = (
     "lbs_abi_version", "lbs_last_error", "lbs_select_tile_len",
+    "lbs_scan_ckpt_len", "lbs_scan_ckpt_bytes",
     "lbs_scan_fwd_workspace_bytes", "lbs_scan_fwd",
     "lbs_scan_bwd_workspace_bytes", "lbs_scan_bwd",
     "lbs_prediscretized_fwd", "lbs_rms_norm_fwd",
@@ -113,6 +114,10 @@ def lib():
     L.lbs_last_error.restype = C.c_char_p
     L.lbs_select_tile_len.restype = I64
     L.lbs_select_tile_len.argtypes = [I64]
+    L.lbs_scan_ckpt_len.restype = I64
+    L.lbs_scan_ckpt_len.argtypes = [I64, I64]
+    L.lbs_scan_ckpt_bytes.restype = C.c_size_t
+    L.lbs_scan_ckpt_bytes.argtypes = [C.POINTER(ScanFwdArgs)]
     L.lbs_scan_fwd_workspace_bytes.restype = C.c_size_t
     L.lbs_scan_fwd_workspace_bytes.argtypes = [C.POINTER(ScanFwdArgs)]
     L.lbs_scan_fwd.restype = C.c_int

@@ -10,6 +10,9 @@
 #include "lbs_common.cuh"
 #include "lbs_internal.h"
 
+extern "C" int64_t lbs_scan_ckpt_len(int64_t seqlen, int64_t window);
+extern "C" size_t lbs_scan_ckpt_bytes(const lbs_scan_fwd_args* a);
+
 namespace {
 
 thread_local std::string g_err;
@@ -80,16 +83,20 @@ int validate_fwd(const lbs_scan_fwd_args* a) {
       return fail(LBS_ERR_UNSUPPORTED, "dtype combination io=%d bc=%d not instantiated (f32/f32, bf16/bf16, bf16/f32)",
                   a->io_dtype, a->bc_dtype);
   }
-  if (!a->u || !a->delta || !a->A || !a->B || !a->C || !a->out)
-    return fail(LBS_ERR_INVALID, "u, delta, A, B, C and out must be non-null");
+  if (!a->u || !a->delta || !a->A || !a->B || !a->C)
+    return fail(LBS_ERR_INVALID, "u, delta, A, B and C must be non-null");
   if (a->dstate > 16)
     return fail(LBS_ERR_UNSUPPORTED, "dstate %lld > 16 is not supported by the fused kernel",
                 (long long)a->dstate);
-  if (a->window > 16 && a->window < a->seqlen)
-    return fail(LBS_ERR_UNSUPPORTED, "window %lld > 16 (with window < L) is not supported yet",
-                (long long)a->window);
-  if (a->checkpoints && (a->ckpt_len < 1 || a->ckpt_len % a->window))
-    return fail(LBS_ERR_INVALID, "ckpt_len must be a positive multiple of the window");
+  {
+    const int64_t m = a->window < a->seqlen ? a->window : a->seqlen;
+    if (m > 16)
+      return fail(LBS_ERR_UNSUPPORTED, "effective window min(window, L) = %lld > 16 is not supported",
+                  (long long)m);
+  }
+  if (a->checkpoints && a->ckpt_len != lbs_scan_ckpt_len(a->seqlen, a->window))
+    return fail(LBS_ERR_INVALID, "ckpt_len %lld != lbs_scan_ckpt_len(L, window) = %lld", (long long)a->ckpt_len,
+                (long long)lbs_scan_ckpt_len(a->seqlen, a->window));
   return LBS_OK;
 }
 
@@ -120,6 +127,57 @@ void fill_fwd_params(const lbs_scan_fwd_args* a, lbs::FwdParams* p) {
   p->ckpt = a->checkpoints;
   p->ckpt_len = (int)a->ckpt_len;
   p->n_ckpt = a->checkpoints ? (int)((a->seqlen + a->ckpt_len - 1) / a->ckpt_len) : 0;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct BwdLayout {
+  int64_t ckpt_len, n_ckpt;
+  size_t off_ckpt, off_seg, off_bc, off_w, total;
+};
+
+int validate_bwd(const lbs_scan_bwd_args* a) {
+  const lbs_scan_fwd_args* f = &a->fwd;
+  if (!a->dout || !a->du || !a->ddelta)
+    return fail(LBS_ERR_INVALID, "dout, du and ddelta must be non-null");
+  if ((a->dz == nullptr) != (f->z == nullptr))
+    return fail(LBS_ERR_INVALID, "dz must be given exactly when z is");
+  if (!a->dA || !a->dB || !a->dC) return fail(LBS_ERR_INVALID, "dA, dB and dC must be non-null");
+  if (a->dD && !f->D) return fail(LBS_ERR_INVALID, "dD given without D");
+  if (a->ddelta_bias && !f->delta_bias) return fail(LBS_ERR_INVALID, "ddelta_bias given without delta_bias");
+  return LBS_OK;
+}
+
+// workspace: [checkpoints (if not supplied)][forward segment aggregates][dB/dC partials][dA/dD/dbias partials]
+int bwd_layout(const lbs_scan_bwd_args* a, BwdLayout* lay) {
+  if (!a) return fail(LBS_ERR_INVALID, "null args");
+  const lbs_scan_fwd_args* f = &a->fwd;
+  int rc = validate_fwd(f);
+  if (rc != LBS_OK) return rc;
+  const int64_t K = lbs_scan_ckpt_len(f->seqlen, f->window);
+  const int64_t nck = (f->seqlen + K - 1) / K;
+  const int NS = padded_states(f->dstate);
+  lay->ckpt_len = K;
+  lay->n_ckpt = nck;
+  size_t off = 0;
+  lay->off_ckpt = off;
+  lay->off_seg = off;
+  if (!f->checkpoints) {
+    off += align256(lbs_scan_ckpt_bytes(f));
+    lay->off_seg = off;
+    lbs_scan_fwd_args b2 = *f;
+    if (b2.window > b2.seqlen) b2.window = b2.seqlen;
+    int S, len;
+    plan_segments(&b2, &S, &len);
+    if (S > 1) off += align256((size_t)f->batch * S * f->dim * 2 * NS * sizeof(float));
+  }
+  const int64_t n_eblk = (f->dim + lbs::kFwdThreads - 1) / lbs::kFwdThreads;
+  lay->off_bc = off;
+  off += align256((size_t)n_eblk * f->batch * f->seqlen * 2 * NS * sizeof(float));
+  lay->off_w = off;
+  off += align256((size_t)f->batch * (NS + 2) * f->dim * sizeof(float));
+  lay->total = off;
+  return LBS_OK;
 }
 
 }  // namespace
@@ -154,9 +212,25 @@ size_t lbs_scan_fwd_workspace_bytes(const lbs_scan_fwd_args* a) {
   return (size_t)a->batch * S * a->dim * 2 * padded_states(a->dstate) * sizeof(float);
 }
 
+int64_t lbs_scan_ckpt_len(int64_t seqlen, int64_t window) {
+  if (seqlen < 1 || window < 1) return -1;
+  const int64_t m = window < seqlen ? window : seqlen;
+  if (m > 16) return -1;
+  return lbs::bwd_chunk_len((int)m);
+}
+
+size_t lbs_scan_ckpt_bytes(const lbs_scan_fwd_args* a) {
+  if (!a || a->batch < 1 || a->seqlen < 1 || a->dim < 1 || a->dstate < 1) return 0;
+  const int64_t K = lbs_scan_ckpt_len(a->seqlen, a->window);
+  if (K < 1) return 0;
+  const int64_t nck = (a->seqlen + K - 1) / K;
+  return (size_t)a->batch * nck * a->dim * padded_states(a->dstate) * sizeof(float);
+}
+
 int lbs_scan_fwd(const lbs_scan_fwd_args* a, void* ws, size_t ws_bytes, void* stream) {
   int rc = validate_fwd(a);
   if (rc != LBS_OK) return rc;
+  if (!a->out && !a->checkpoints) return fail(LBS_ERR_INVALID, "out must be non-null");
   lbs::FwdParams p{};
   fill_fwd_params(a, &p);
   lbs_scan_fwd_args b = *a;
@@ -168,7 +242,6 @@ int lbs_scan_fwd(const lbs_scan_fwd_args* a, void* ws, size_t ws_bytes, void* st
       return fail(LBS_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
     p.seg_agg = static_cast<float*>(ws);
   }
-  if (p.ckpt) return fail(LBS_ERR_UNSUPPORTED, "forward checkpoints not implemented yet");
   return cuda_status(lbs::launch_fwd(p, a->io_dtype, a->bc_dtype, (cudaStream_t)stream), "lbs_scan_fwd");
 }
 
@@ -210,13 +283,64 @@ int lbs_rms_norm_fwd(const lbs_norm_args* a, void* stream) {
 }
 
 size_t lbs_scan_bwd_workspace_bytes(const lbs_scan_bwd_args* a) {
-  (void)a;
-  return 0;
+  BwdLayout lay;
+  if (bwd_layout(a, &lay) != LBS_OK) return 0;
+  return lay.total;
 }
 
 int lbs_scan_bwd(const lbs_scan_bwd_args* a, void* ws, size_t ws_bytes, void* stream) {
-  (void)a; (void)ws; (void)ws_bytes; (void)stream;
-  return fail(LBS_ERR_UNSUPPORTED, "lbs_scan_bwd not implemented yet");
+  BwdLayout lay;
+  int rc = bwd_layout(a, &lay);
+  if (rc != LBS_OK) return rc;
+  rc = validate_bwd(a);
+  if (rc != LBS_OK) return rc;
+  if (lay.total && (!ws || ws_bytes < lay.total))
+    return fail(LBS_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", lay.total, ws_bytes);
+  char* w = static_cast<char*>(ws);
+  cudaStream_t st = (cudaStream_t)stream;
+  const lbs_scan_fwd_args* f = &a->fwd;
+  lbs::BwdParams P{};
+  fill_fwd_params(f, &P.f);
+  P.f.out = nullptr;
+  P.f.last_state = nullptr;
+  P.f.n_seg = 1;
+  P.f.seg_len = P.f.L;
+  P.f.seg_agg = nullptr;
+  P.f.ckpt_len = (int)lay.ckpt_len;
+  P.f.n_ckpt = (int)lay.n_ckpt;
+  if (f->checkpoints) {
+    P.f.ckpt = f->checkpoints;
+  } else {
+    // checkpoint-only forward sweep (no LB pass, no output) into the workspace
+    P.f.ckpt = reinterpret_cast<float*>(w + lay.off_ckpt);
+    lbs::FwdParams fp = P.f;
+    fp.flags &= ~LBS_FLAG_LB;
+    fp.z = lbs::View3D{nullptr, 0, 0, 0};
+    lbs_scan_fwd_args b2 = *f;
+    b2.window = fp.m;
+    plan_segments(&b2, &fp.n_seg, &fp.seg_len);
+    if (fp.n_seg > 1) fp.seg_agg = reinterpret_cast<float*>(w + lay.off_seg);
+    rc = cuda_status(lbs::launch_fwd(fp, f->io_dtype, f->bc_dtype, st), "lbs_scan_bwd (recompute)");
+    if (rc != LBS_OK) return rc;
+  }
+  P.dout = view(a->dout, a->dout_stride);
+  P.du = lbs::OutView{a->du, a->du_stride[0], a->du_stride[1], a->du_stride[2]};
+  P.ddelta = lbs::OutView{a->ddelta, a->ddelta_stride[0], a->ddelta_stride[1], a->ddelta_stride[2]};
+  P.dz = lbs::OutView{a->dz, a->dz_stride[0], a->dz_stride[1], a->dz_stride[2]};
+  P.part_bc = reinterpret_cast<float*>(w + lay.off_bc);
+  P.part_w = reinterpret_cast<float*>(w + lay.off_w);
+  P.dA = a->dA;
+  P.dD = a->dD;
+  P.dbias = a->ddelta_bias;
+  P.dB = a->dB;
+  P.sb0 = a->dB_stride[0];
+  P.sb1 = a->dB_stride[1];
+  P.sb2 = a->dB_stride[2];
+  P.dC = a->dC;
+  P.sc0 = a->dC_stride[0];
+  P.sc1 = a->dC_stride[1];
+  P.sc2 = a->dC_stride[2];
+  return cuda_status(lbs::launch_bwd(P, f->io_dtype, f->bc_dtype, st), "lbs_scan_bwd");
 }
 
 }  // extern "C"

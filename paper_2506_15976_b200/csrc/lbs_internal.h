@@ -35,6 +35,33 @@ struct FwdParams {
 cudaError_t launch_fwd(const FwdParams& p, int io_dtype, int bc_dtype, cudaStream_t st);
 int fwd_padded_states(int N);  // NS used by the kernels for a given N
 
+struct OutView {
+  void* p;
+  long long s0, s1, s2;
+};
+
+// Backward: the forward's parameters (f.out unused) plus gradients.
+// f.ckpt must hold the checkpoints (state entering every bwd chunk of
+// f.ckpt_len steps) — written by the forward or by a checkpoint-only sweep.
+struct BwdParams {
+  FwdParams f;
+  View3D dout;
+  OutView du, ddelta, dz;  // io dtype; dz.p == nullptr iff no gate
+  float* part_bc;          // [n_eblk][Bt][L][2][NS] dB/dC partials per channel block
+  float* part_w;           // [Bt][NS+2][E] per-row dA (NS), dD, ddelta_bias partials
+  // final outputs (reduction kernel)
+  float* dA;               // (E, N)  +=
+  float* dD;               // (E) or nullptr, +=
+  float* dbias;            // (E) or nullptr, +=
+  float* dB;
+  long long sb0, sb1, sb2;
+  float* dC;
+  long long sc0, sc1, sc2;
+};
+
+cudaError_t launch_bwd(const BwdParams& p, int io_dtype, int bc_dtype, cudaStream_t st);
+int bwd_chunk_len(int m);  // steps per backward chunk (= checkpoint spacing) for window m
+
 struct PreParams {
   int Bt, L, E, N, m;
   uint32_t flags;

@@ -1,0 +1,519 @@
+// Fused LB selective scan — backward (sm_100a).
+//
+// Replaces the reference's adjoint kernel autodiff._scan_grad_kernel
+// (autodiff.py:48-159, restated in oracle/lbscan_oracle.py:lbm_scan_grad),
+// chained in the same launch through block._discretize_backward
+// (block.py:106-129) and the gate adjoint (block.py:199-200).  Nothing of
+// size (B,L,E,N) touches HBM: per (b,l) the kernel reads u, delta, z, dout (E
+// each) and B, C (N each) and writes du, ddelta, dz (E each) plus fp32 dB/dC
+// partial sums (2N per channel block).
+//
+// Math per lane (b,e,n), t in scanned order (a = exp(dl*A), b = dl*u*B,
+// g = C*gy, gy = dout*silu(z)):
+//   forward adjoint  lam_t = g_t + a_{t+1} lam_{t+1}      -> dbx_t = lam_t, dabar_t = lam_t h_{t-1}
+//   tile-local LB    v_i = g_i + a_{i-1} v_{i-1} (ascending in a tile, v_lo = g_lo)
+//                    dabar_i += v_i (r_{i+1} + b_{i+1})     (i not a tile end)
+//                    dbx_{i+1} += a_i v_i                  (i+1 not a tile start)
+//   chain            ddl = sum_n dabar a A + u sum_n dbx B;  du = D gy + dl sum_n dbx B
+//                    dA += dabar a dl;  dB = sum_e dbx dl u;  dC = sum_e gy (h + r)
+//                    ddelta = ddl * sigmoid(delta + bias);   dz = dout y silu'(z)
+//
+// Execution model: one thread owns one (b, e) channel (128 channels per CTA,
+// like the forward) and walks the sequence BACKWARDS in chunks of K steps
+// (K = whole LB tiles, K <= KT registers).  The state entering every chunk
+// comes from checkpoints (written by the training forward, or by a
+// checkpoint-only forward sweep), staged into shared memory with cp.async one
+// chunk ahead together with u/delta/z/dout rows and B/C.  Inside a chunk the
+// loop runs state-pair-outer: for each pair (n, n+1) an ascending pass
+// recomputes a, h and the LB adjoint v in registers, and a descending pass
+// runs the LB record r (as Q = r + b), the global adjoint lam and all chain
+// terms with packed FFMA2.  lam crosses chunk boundaries through shared
+// memory.  The E-reductions for dB/dC are a warp reduce-scatter (16 values
+// per 16 shuffles) + a 4-warp smem sum, written as per-CTA partials and
+// reduced deterministically by a second kernel (no atomics: the reference's
+// partial-then-reduce order, autodiff.py:182,188).
+#pragma once
+#include "lbs_scan_fwd.cuh"
+
+namespace lbs {
+
+constexpr int kBwdThreads = kFwdThreads;  // BcPrefetch assumes 128 threads
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+
+template <typename Tio, int NS, int KT>
+struct BwdSmem {
+  static constexpr int NP = NS / 2;
+  static constexpr size_t seq_bytes = 2ull * 4 * KT * kBwdThreads * sizeof(Tio);  // u, delta, z, dout
+  static constexpr size_t bc_bytes = (size_t)KT * 2 * NS * sizeof(float);
+  static constexpr size_t ck_bytes = 2ull * NP * kBwdThreads * sizeof(f2);
+  static constexpr size_t pq_bytes = (size_t)NP * kBwdThreads * sizeof(f2);  // a2s, mu, dA each
+  static constexpr size_t red_bytes = 4ull * KT * 2 * NS * sizeof(float);
+  static constexpr size_t off_bc = seq_bytes;
+  static constexpr size_t off_ck = off_bc + bc_bytes;
+  static constexpr size_t off_a2 = off_ck + ck_bytes;
+  static constexpr size_t off_mu = off_a2 + pq_bytes;
+  static constexpr size_t off_da = off_mu + pq_bytes;
+  static constexpr size_t off_red = off_da + pq_bytes;
+  static constexpr size_t total = off_red + red_bytes;
+};
+
+// u / delta / z / dout rows of one chunk -> ring stage (see SeqStager).
+template <typename Tio, bool kVec, int KT>
+struct BwdStager {
+  static constexpr int PPR = kBwdThreads * sizeof(Tio) / 16;
+  static constexpr int EPP = 16 / sizeof(Tio);
+  static constexpr int RS = kBwdThreads / PPR;
+  static constexpr int KP = (KT + RS - 1) / RS;
+  const Tio* base[4];
+  long long step[4];
+  int row0, col;
+  bool ok;
+  __device__ __forceinline__ void init(const View3D* const* v, int L, bool rev, int b, int e0, int E) {
+    if constexpr (kVec) {
+      row0 = threadIdx.x / PPR;
+      col = (threadIdx.x % PPR) * EPP;
+    } else {
+      row0 = 0;
+      col = threadIdx.x;
+    }
+    ok = e0 + col < E;
+    const int ec = ok ? e0 + col : 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const View3D& w = *v[a];
+      base[a] = w.p ? static_cast<const Tio*>(w.p) + (long long)b * w.s0 + (long long)ec * w.s2 +
+                          (rev ? (long long)(L - 1) * w.s1 : 0)
+                    : nullptr;
+      step[a] = rev ? -w.s1 : w.s1;
+    }
+  }
+  __device__ __forceinline__ void issue(Tio* seq, int stg, int c, int clen) const {
+    if (!ok) return;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      if (base[a] == nullptr) continue;
+      Tio* dst = seq + ((size_t)(stg * 4 + a) * KT) * kBwdThreads + col;
+      if constexpr (kVec) {
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int t = row0 + k * RS;
+          if (t < clen) cp_async16(dst + t * kBwdThreads, base[a] + (long long)(c + t) * step[a]);
+        }
+      } else {
+        for (int t = 0; t < clen; ++t) dst[t * kBwdThreads] = base[a][(long long)(c + t) * step[a]];
+      }
+    }
+  }
+};
+
+// Warp reduce-scatter of 16 values: returns, in lane l, the warp sum of value
+// index (l >> 1) (lanes l and l^1 hold the same sum).  16 shuffles total.
+__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool hi = lane & 16;
+    const float send = hi ? v[i] : v[i + 8];
+    const float keep = hi ? v[i + 8] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 8;
+    const float send = hi ? v[i] : v[i + 4];
+    const float keep = hi ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 4;
+    const float send = hi ? v[i] : v[i + 2];
+    const float keep = hi ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool hi = lane & 2;
+    const float send = hi ? v[0] : v[1];
+    const float keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+struct BwdChunkCtx {
+  int c, clen, L, m, stg;
+  unsigned tstart, tend;  // bit j: step j starts / ends an LB tile
+  bool active, has_z, softplus, linear;
+  float Dv, bias;
+};
+
+template <typename Tio, int NS, int KT, bool kLB, bool kFull>
+__device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx& x, const Tio* su,
+                                          const Tio* sd, const Tio* sz, const Tio* sg,
+                                          const float* bcf, const f2* ck, const f2* a2s, f2* mu,
+                                          f2* dAs, float* red, float& dD_acc, float& dbias_acc,
+                                          Tio* dup, Tio* ddp, Tio* dzp, long long sdu, long long sdd,
+                                          long long sdz) {
+  constexpr int NP = NS / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int clen = x.clen;
+  float dl[KT], dlu[KT], gy[KT];
+  f2 Y[KT], Pacc[KT], S[KT];
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    const bool on = kFull || j < clen;
+    float d = on ? to_f(sd[j * kBwdThreads + tid]) + x.bias : 0.f;
+    const float uv = on ? to_f(su[j * kBwdThreads + tid]) : 0.f;
+    if (x.softplus) d = softplus_f(d);
+    float g = (on && x.active) ? to_f(sg[j * kBwdThreads + tid]) : 0.f;
+    if (x.has_z && on) g *= silu_f(to_f(sz[j * kBwdThreads + tid]));
+    dl[j] = on ? d : 0.f;
+    dlu[j] = on ? d * uv : 0.f;
+    gy[j] = g;
+    Y[j] = mk2(0.f, 0.f);
+    Pacc[j] = mk2(0.f, 0.f);
+    S[j] = mk2(0.f, 0.f);
+  }
+  const int jlast = kFull ? KT - 1 : clen - 1;
+
+#pragma unroll 1
+  for (int q = 0; q < NP; ++q) {
+    const f2 A2 = a2s[q * kBwdThreads + tid];
+    const f2 h0 = ck[q * kBwdThreads + tid];
+    const f2 mu_in = mu[q * kBwdThreads + tid];
+    f2 a[KT], h[KT], v[KT];
+    // ---- ascending: a, h (state recompute from the checkpoint), LB adjoint v
+    f2 hp = h0;
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      if (kFull || j < clen) {
+        const f2 xa = mul2(bc2(dl[j]), A2);
+        a[j] = x.linear ? xa : mk2(ex2(xa.x), ex2(xa.y));
+        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + 2 * q]);
+        hp = fma2(a[j], hp, mul2(bc2(dlu[j]), Bv));
+        h[j] = hp;
+        if (kLB) {
+          const f2 Cv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + NS + 2 * q]);
+          const f2 g = mul2(bc2(gy[j]), Cv);
+          v[j] = (j == 0 || ((x.tstart >> j) & 1u)) ? g : fma2(a[j > 0 ? j - 1 : 0], v[j > 0 ? j - 1 : 0], g);
+        }
+      } else {
+        a[j] = mk2(0.f, 0.f);
+        h[j] = mk2(0.f, 0.f);
+        v[j] = mk2(0.f, 0.f);
+      }
+    }
+    // ---- descending: LB record Q = r + b, adjoint lam, chain terms
+    f2 Qn = mk2(0.f, 0.f), lam = mk2(0.f, 0.f), dAq = mk2(0.f, 0.f);
+    float rv[16];
+#pragma unroll
+    for (int j = KT - 1; j >= 0; --j) {
+      f2 dBv = mk2(0.f, 0.f), dCv = mk2(0.f, 0.f);
+      if (kFull || j < clen) {
+        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + 2 * q]);
+        const f2 Cv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + NS + 2 * q]);
+        const f2 bj = mul2(bc2(dlu[j]), Bv);
+        const f2 g = mul2(bc2(gy[j]), Cv);
+        const bool tend = (x.tend >> j) & 1u;
+        const bool tstart = j == 0 || ((x.tstart >> j) & 1u);
+        f2 hr = h[j], Qc = bj;
+        if (kLB && !tend) {
+          hr = fma2(a[j], Qn, h[j]);
+          Qc = fma2(a[j], Qn, bj);
+        }
+        const f2 lamj = (j == jlast) ? add2(g, mu_in) : fma2(a[j < KT - 1 ? j + 1 : j], lam, g);
+        const f2 hprev = j > 0 ? h[j > 0 ? j - 1 : 0] : h0;
+        f2 dab = mul2(lamj, hprev);
+        if (kLB && !tend) dab = fma2(v[j], Qn, dab);
+        f2 dbx = lamj;
+        if (kLB && !tstart) dbx = fma2(a[j > 0 ? j - 1 : 0], v[j > 0 ? j - 1 : 0], dbx);
+        const f2 da = x.linear ? dab : mul2(dab, a[j]);
+        Pacc[j] = fma2(da, A2, Pacc[j]);
+        dAq = fma2(da, bc2(dl[j]), dAq);
+        S[j] = fma2(dbx, Bv, S[j]);
+        if (x.has_z) Y[j] = fma2(Cv, hr, Y[j]);
+        dBv = mul2(dbx, bc2(dlu[j]));
+        dCv = mul2(hr, bc2(gy[j]));
+        lam = lamj;
+        Qn = Qc;
+      }
+      const int o = (j & 3) * 4;
+      rv[o + 0] = dBv.x;
+      rv[o + 1] = dBv.y;
+      rv[o + 2] = dCv.x;
+      rv[o + 3] = dCv.y;
+      if ((j & 3) == 0) {
+        const float s = reduce_scatter16(rv, lane);
+        if ((lane & 1) == 0) {
+          const int idx = lane >> 1;
+          const int jj = j + (idx >> 2), kind = idx & 3;
+          red[((warp * KT + jj) * 2 + (kind >> 1)) * NS + 2 * q + (kind & 1)] = s;
+        }
+      }
+    }
+    // carry into the previous chunk: a_{c} * lam_{c}
+    mu[q * kBwdThreads + tid] = mul2(a[0], lam);
+    dAs[q * kBwdThreads + tid] = add2(dAs[q * kBwdThreads + tid], dAq);
+  }
+
+  // ---- per-step outputs: du, ddelta, dz
+  if (x.active) {
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      if (kFull || j < clen) {
+        const float uv = to_f(su[j * kBwdThreads + tid]);
+        const float s = S[j].x + S[j].y;
+        const float duv = x.Dv * gy[j] + dl[j] * s;
+        const float pp = (Pacc[j].x + Pacc[j].y) * (x.linear ? 1.f : kLn2);
+        const float ddl = pp + uv * s;
+        const float dpre = to_f(sd[j * kBwdThreads + tid]) + x.bias;
+        const float ddv = x.softplus ? ddl * sigmoid_f(dpre) : ddl;
+        dbias_acc += ddv;
+        dD_acc += gy[j] * uv;
+        const long long t = x.c + j;
+        st<Tio>(dup + t * sdu, duv);
+        st<Tio>(ddp + t * sdd, ddv);
+        if (x.has_z) {
+          const float y = Y[j].x + Y[j].y + x.Dv * uv;
+          const float zv = to_f(sz[j * kBwdThreads + tid]);
+          const float sgm = sigmoid_f(zv);
+          const float go = to_f(sg[j * kBwdThreads + tid]);
+          st<Tio>(dzp + t * sdz, go * y * sgm * (1.f + zv * (1.f - sgm)));
+        }
+      }
+    }
+  }
+}
+
+template <typename Tio, typename Tbc, int NS, int KT, bool kLB, bool kVec>
+__global__ void __launch_bounds__(kBwdThreads, 1) bwd_kernel(BwdParams P) {
+  constexpr int NP = NS / 2;
+  using Sm = BwdSmem<Tio, NS, KT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tio* seq = reinterpret_cast<Tio*>(smem_raw);
+  float* bcf = reinterpret_cast<float*>(smem_raw + Sm::off_bc);
+  f2* cks = reinterpret_cast<f2*>(smem_raw + Sm::off_ck);
+  f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::off_a2);
+  f2* mus = reinterpret_cast<f2*>(smem_raw + Sm::off_mu);
+  f2* dAs = reinterpret_cast<f2*>(smem_raw + Sm::off_da);
+  float* red = reinterpret_cast<float*>(smem_raw + Sm::off_red);
+
+  const FwdParams& p = P.f;
+  const int tid = threadIdx.x;
+  const int e0 = blockIdx.x * kBwdThreads;
+  const int e = e0 + tid;
+  const int b = blockIdx.y;
+  const bool active = e < p.E;
+  const int ec = active ? e : p.E - 1;
+  const int L = p.L, N = p.N, m = p.m, K = p.ckpt_len, nck = p.n_ckpt;
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool linear = p.flags & LBS_FLAG_LINEAR;
+  const bool has_z = p.z.p != nullptr;
+
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    float a0 = 2 * q < N ? p.A[(long long)ec * N + 2 * q] : 0.f;
+    float a1 = 2 * q + 1 < N ? p.A[(long long)ec * N + 2 * q + 1] : 0.f;
+    if (!linear) { a0 *= kLog2e; a1 *= kLog2e; }
+    a2s[q * kBwdThreads + tid] = mk2(a0, a1);
+    mus[q * kBwdThreads + tid] = mk2(0.f, 0.f);
+    dAs[q * kBwdThreads + tid] = mk2(0.f, 0.f);
+  }
+  BwdChunkCtx x;
+  x.L = L;
+  x.m = m;
+  x.active = active;
+  x.has_z = has_z;
+  x.softplus = p.flags & LBS_FLAG_SOFTPLUS;
+  x.linear = linear;
+  x.Dv = p.D ? p.D[ec] : 0.f;
+  x.bias = p.bias ? p.bias[ec] : 0.f;
+  float dD_acc = 0.f, dbias_acc = 0.f;
+
+  // output row bases (flip-on-store for the reverse direction)
+  auto obase = [&](const OutView& o) -> Tio* {
+    if (o.p == nullptr) return nullptr;
+    return static_cast<Tio*>(o.p) + (long long)b * o.s0 + (long long)ec * o.s2 + (rev ? (long long)(L - 1) * o.s1 : 0);
+  };
+  Tio* dup = obase(P.du);
+  Tio* ddp = obase(P.ddelta);
+  Tio* dzp = obase(P.dz);
+  const long long sdu = rev ? -P.du.s1 : P.du.s1;
+  const long long sdd = rev ? -P.ddelta.s1 : P.ddelta.s1;
+  const long long sdz = rev ? -P.dz.s1 : P.dz.s1;
+
+  const View3D zv = has_z ? p.z : View3D{nullptr, 0, 0, 0};
+  const View3D* views[4] = {&p.u, &p.delta, &zv, &P.dout};
+  BwdStager<Tio, kVec, KT> stager;
+  stager.init(views, L, rev, b, e0, p.E);
+  BcPrefetch<Tbc, NS, KT> bcpre;
+  bcpre.init(p, b);
+  const f2* ckg = reinterpret_cast<const f2*>(p.ckpt) + (long long)b * nck * NP * p.E + ec;
+  auto ck_issue = [&](int stg, int k) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+      cp_async8(&cks[(stg * NP + q) * kBwdThreads + tid], ckg + ((long long)k * NP + q) * p.E);
+  };
+
+  int k = nck - 1;
+  int c = k * K;
+  int clen = L - c;
+  stager.issue(seq, 0, c, clen);
+  ck_issue(0, k);
+  cp_async_commit();
+  bcpre.load(c, clen);
+  const int eblk = blockIdx.x;
+  for (int it = 0; k >= 0; ++it, --k) {
+    const int stg = it & 1;
+    cp_async_wait_all();
+    __syncthreads();  // chunk k landed; chunk k+1 compute (and its partial write) done
+    bcpre.publish(bcf);
+    if (k > 0) {
+      stager.issue(seq, stg ^ 1, c - K, K);
+      ck_issue(stg ^ 1, k - 1);
+      bcpre.load(c - K, K);
+    }
+    cp_async_commit();
+    __syncthreads();  // bcf visible
+
+    x.c = c;
+    x.clen = clen;
+    x.stg = stg;
+    unsigned ts = 0u, te = 0u;
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      if (j < clen) {
+        const int lt = c + j;
+        if (lt % m == 0) ts |= 1u << j;
+        if ((lt + 1) % m == 0 || lt == L - 1) te |= 1u << j;
+      }
+    }
+    x.tstart = ts;
+    x.tend = te;
+    const Tio* base = seq + (size_t)stg * 4 * KT * kBwdThreads;
+    const Tio* su = base;
+    const Tio* sd = base + KT * kBwdThreads;
+    const Tio* sz = base + 2 * KT * kBwdThreads;
+    const Tio* sg = base + 3 * KT * kBwdThreads;
+    const f2* ck = cks + stg * NP * kBwdThreads;
+    if (clen == KT)
+      bwd_chunk<Tio, NS, KT, kLB, true>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, dD_acc, dbias_acc,
+                                        dup, ddp, dzp, sdu, sdd, sdz);
+    else
+      bwd_chunk<Tio, NS, KT, kLB, false>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, dD_acc, dbias_acc,
+                                         dup, ddp, dzp, sdu, sdd, sdz);
+    __syncthreads();  // red complete
+    // dB / dC partials of this channel block: sum the 4 warps
+    for (int i = tid; i < KT * 2 * NS; i += kBwdThreads) {
+      const int j = i / (2 * NS);
+      if (j < clen) {
+        const float s = red[i] + red[KT * 2 * NS + i] + red[2 * KT * 2 * NS + i] + red[3 * KT * 2 * NS + i];
+        P.part_bc[(((long long)eblk * p.Bt + b) * L + (c + j)) * (2 * NS) + (i - j * 2 * NS)] = s;
+      }
+    }
+    c -= K;
+    clen = K;
+  }
+  if (active) {
+    float* pw = P.part_w + (long long)b * (NS + 2) * p.E + e;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const f2 d = dAs[q * kBwdThreads + tid];
+      pw[(long long)(2 * q) * p.E] = d.x;
+      pw[(long long)(2 * q + 1) * p.E] = d.y;
+    }
+    pw[(long long)NS * p.E] = dD_acc;
+    pw[(long long)(NS + 1) * p.E] = dbias_acc;
+  }
+}
+
+// Deterministic reductions of the partials (fixed order, fp64 accumulate).
+template <int NS>
+__global__ void bwd_reduce_bc_kernel(BwdParams P, int n_eblk) {
+  const FwdParams& p = P.f;
+  const long long total = (long long)p.Bt * p.L * 2 * p.N;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int n = idx % p.N;
+  const int which = (idx / p.N) % 2;
+  const long long bt = idx / (2 * p.N);
+  const int t = bt % p.L;
+  const int b = bt / p.L;
+  double s = 0.0;
+  for (int k = 0; k < n_eblk; ++k)
+    s += P.part_bc[(((long long)k * p.Bt + b) * p.L + t) * (2 * NS) + which * NS + n];
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const long long tp = rev ? (p.L - 1 - t) : t;
+  if (which == 0)
+    P.dB[b * P.sb0 + tp * P.sb1 + n * P.sb2] = (float)s;
+  else
+    P.dC[b * P.sc0 + tp * P.sc1 + n * P.sc2] = (float)s;
+}
+
+template <int NS>
+__global__ void bwd_reduce_w_kernel(BwdParams P) {
+  const FwdParams& p = P.f;
+  const int total = p.E * (p.N + 2);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int e = idx % p.E;
+  const int i = idx / p.E;
+  const int row = i < p.N ? i : NS + (i - p.N);
+  double s = 0.0;
+  for (int b = 0; b < p.Bt; ++b) s += P.part_w[((long long)b * (NS + 2) + row) * p.E + e];
+  if (i < p.N)
+    P.dA[(long long)e * p.N + i] += (float)s;
+  else if (i == p.N) {
+    if (P.dD) P.dD[e] += (float)s;
+  } else if (P.dbias) {
+    P.dbias[e] += (float)s;
+  }
+}
+
+template <typename Tio, typename Tbc, int NS, int KT, bool kVec>
+inline cudaError_t launch_bwd_t(const BwdParams& P, cudaStream_t st) {
+  const size_t smem = BwdSmem<Tio, NS, KT>::total;
+  const FwdParams& p = P.f;
+  const int n_eblk = (p.E + kBwdThreads - 1) / kBwdThreads;
+  dim3 grid(n_eblk, p.Bt);
+  auto k = (p.flags & LBS_FLAG_LB) ? bwd_kernel<Tio, Tbc, NS, KT, true, kVec>
+                                   : bwd_kernel<Tio, Tbc, NS, KT, false, kVec>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<grid, kBwdThreads, smem, st>>>(P);
+  const long long nbc = (long long)p.Bt * p.L * 2 * p.N;
+  bwd_reduce_bc_kernel<NS><<<(unsigned)((nbc + 255) / 256), 256, 0, st>>>(P, n_eblk);
+  const int nw = p.E * (p.N + 2);
+  bwd_reduce_w_kernel<NS><<<(nw + 255) / 256, 256, 0, st>>>(P);
+  return cudaGetLastError();
+}
+
+template <typename Tio, typename Tbc, int NS, bool kVec>
+inline cudaError_t launch_bwd_m(const BwdParams& P, cudaStream_t st) {
+  if (P.f.m <= 8) return launch_bwd_t<Tio, Tbc, NS, 8, kVec>(P, st);
+  return launch_bwd_t<Tio, Tbc, NS, 16, kVec>(P, st);
+}
+
+template <typename Tio, typename Tbc, bool kVec>
+inline cudaError_t launch_bwd_n(const BwdParams& P, cudaStream_t st) {
+  if (P.f.N <= 4) return launch_bwd_m<Tio, Tbc, 4, kVec>(P, st);
+  return launch_bwd_m<Tio, Tbc, 16, kVec>(P, st);
+}
+
+template <typename Tio, typename Tbc>
+inline cudaError_t launch_bwd_v(const BwdParams& P, cudaStream_t st) {
+  const size_t es = sizeof(Tio);
+  const int epp = 16 / (int)es;
+  auto ok = [&](const View3D& v) {
+    if (!v.p) return true;
+    return v.s2 == 1 && (reinterpret_cast<uintptr_t>(v.p) % 16) == 0 && (v.s0 * es) % 16 == 0 &&
+           (v.s1 * es) % 16 == 0;
+  };
+  const bool vec = P.f.E % epp == 0 && ok(P.f.u) && ok(P.f.delta) && ok(P.f.z) && ok(P.dout);
+  return vec ? launch_bwd_n<Tio, Tbc, true>(P, st) : launch_bwd_n<Tio, Tbc, false>(P, st);
+}
+
+}  // namespace lbs

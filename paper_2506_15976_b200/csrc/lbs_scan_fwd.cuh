@@ -296,8 +296,10 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? 4 : 2)) fwd_kernel(Fwd
     }
   }
 
-  Tio* op = static_cast<Tio*>(p.out) + (long long)b * p.so0 + (long long)ec * p.so2 +
-            (rev ? (long long)(L - 1) * p.so1 : 0);
+  // p.out == nullptr: checkpoint-only sweep (the backward's recompute pass)
+  Tio* op = p.out == nullptr ? nullptr
+                             : static_cast<Tio*>(p.out) + (long long)b * p.so0 + (long long)ec * p.so2 +
+                                   (rev ? (long long)(L - 1) * p.so1 : 0);
   const long long ostep = rev ? -p.so1 : p.so1;
 
   SeqStager<Tio, kVec> stager;
@@ -328,9 +330,17 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? 4 : 2)) fwd_kernel(Fwd
     const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * kFwdThreads;
     const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * kFwdThreads;
     const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * kFwdThreads;
-    const TileOut o{op, ostep, c, active, has_z, Dv};
+    const TileOut o{op, ostep, c, active && p.out != nullptr, has_z, Dv};
     for (int t0 = 0; t0 < clen; t0 += m) {
       const int r = min(m, clen - t0);
+      if (p.ckpt != nullptr && active && (c + t0) % p.ckpt_len == 0) {
+        // training checkpoint: state entering backward chunk (c+t0)/ckpt_len,
+        // layout [b][chunk][pair q][e] (f2) — coalesced across the warp
+        f2* ck = reinterpret_cast<f2*>(p.ckpt) +
+                 (((long long)b * p.n_ckpt + (c + t0) / p.ckpt_len) * NP) * p.E + e;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) ck[(long long)q * p.E] = h[q];
+      }
       if (r == MT)
         tile_compute<Tio, NS, MT, kLB, true>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
       else

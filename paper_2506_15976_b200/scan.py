@@ -139,8 +139,10 @@ def _flags(delta_softplus, reverse, lb, mode):
 def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
                            delta_softplus=True, window=None, reverse=False,
                            return_last_state=False, lb=True, discretize_mode="exp",
-                           out=None, seg_hint=0):
-    """Forward launch (no autograd).  Returns ``out`` or ``(out, last_state)``."""
+                           out=None, seg_hint=0, save_checkpoints=False):
+    """Forward launch (no autograd).  Returns ``out`` or ``(out, last_state)``;
+    with ``save_checkpoints`` a trailing fp32 checkpoint buffer for
+    :func:`lbm_selective_scan_bwd` is appended."""
     u, delta, A, B, C, D, z, delta_bias, M, dims = _prepare(u, delta, A, B, C, D, z, delta_bias, window)
     Bt, L, E, N = dims
     if out is None:
@@ -149,37 +151,97 @@ def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
     flags = _flags(delta_softplus, reverse, lb, discretize_mode)
     args = _fwd_args(u, delta, A, B, C, D, z, delta_bias, M, dims, flags, out, last, seg_hint)
     L_ = _lib.lib()
+    ck = None
+    if save_checkpoints:
+        nck = L_.lbs_scan_ckpt_bytes(ctypes.byref(args))
+        if nck == 0:
+            raise NotImplementedError(f"lbm_selective_scan: no checkpoint plan for L={L}, window={M}")
+        ck = torch.empty(nck // 4, dtype=torch.float32, device=u.device)
+        args.checkpoints = ck.data_ptr()
+        args.ckpt_len = L_.lbs_scan_ckpt_len(L, M)
     nws = L_.lbs_scan_fwd_workspace_bytes(ctypes.byref(args))
     ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=u.device) if nws else None
     rc = L_.lbs_scan_fwd(ctypes.byref(args), _ptr(ws), nws, _stream())
     _lib.check(rc, "lbm_selective_scan")
-    return (out, last) if return_last_state else out
+    res = (out, last) if return_last_state else (out,)
+    if save_checkpoints:
+        res = res + (ck,)
+    return res if len(res) > 1 else res[0]
+
+
+def lbm_selective_scan_bwd(dout, u, delta, A, B, C, D=None, z=None, delta_bias=None,
+                           delta_softplus=True, window=None, reverse=False, lb=True,
+                           discretize_mode="exp", checkpoints=None):
+    """Backward launch (lbs_scan_bwd): the adjoint of :func:`lbm_selective_scan_fwd`
+    (autodiff.lbm_scan_grad, autodiff.py:192-195, chained through
+    block._discretize_backward, block.py:106-129, and the gate).
+
+    Returns a dict ``du, ddelta, dz`` (io dtype, ``dz`` None without ``z``),
+    ``dA`` (E, N), ``dD``, ``ddelta_bias`` (E,) and ``dB``, ``dC`` (B, L, N), all
+    fp32.  ``checkpoints`` is the buffer from ``save_checkpoints=True`` (else the
+    states are recomputed by a checkpoint-only forward sweep)."""
+    u, delta, A, B, C, D, z, delta_bias, M, dims = _prepare(u, delta, A, B, C, D, z, delta_bias, window)
+    Bt, L, E, N = dims
+    _need_cuda("dout", dout)
+    if dout.shape != u.shape:
+        raise ShapeError(f"dout has shape {tuple(dout.shape)}, expected {tuple(u.shape)}")
+    dout = dout.to(u.dtype)
+    flags = _flags(delta_softplus, reverse, lb, discretize_mode)
+    dev = u.device
+    a = _lib.ScanBwdArgs()
+    a.fwd = _fwd_args(u, delta, A, B, C, D, z, delta_bias, M, dims, flags, None, None)
+    L_ = _lib.lib()
+    if checkpoints is not None:
+        a.fwd.checkpoints = checkpoints.data_ptr()
+        a.fwd.ckpt_len = L_.lbs_scan_ckpt_len(L, M)
+    du = torch.empty((Bt, L, E), dtype=u.dtype, device=dev)
+    ddelta = torch.empty((Bt, L, E), dtype=u.dtype, device=dev)
+    dz = torch.empty((Bt, L, E), dtype=u.dtype, device=dev) if z is not None else None
+    dA = torch.zeros((E, N), dtype=torch.float32, device=dev)
+    dD = torch.zeros(E, dtype=torch.float32, device=dev) if D is not None else None
+    dbias = torch.zeros(E, dtype=torch.float32, device=dev) if delta_bias is not None else None
+    dB = torch.empty((Bt, L, N), dtype=torch.float32, device=dev)
+    dC = torch.empty((Bt, L, N), dtype=torch.float32, device=dev)
+    a.dout, a.dout_stride = _ptr(dout), _strides(dout)
+    a.du, a.du_stride = _ptr(du), _strides(du)
+    a.ddelta, a.ddelta_stride = _ptr(ddelta), _strides(ddelta)
+    a.dz, a.dz_stride = _ptr(dz), _strides(dz)
+    a.dA, a.dD, a.ddelta_bias = _ptr(dA), _ptr(dD), _ptr(dbias)
+    a.dB, a.dB_stride = _ptr(dB), _strides(dB)
+    a.dC, a.dC_stride = _ptr(dC), _strides(dC)
+    nws = L_.lbs_scan_bwd_workspace_bytes(ctypes.byref(a))
+    ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=dev)
+    rc = L_.lbs_scan_bwd(ctypes.byref(a), _ptr(ws), nws, _stream())
+    _lib.check(rc, "lbm_selective_scan_bwd")
+    return dict(du=du, ddelta=ddelta, dA=dA, dB=dB, dC=dC, dD=dD, dz=dz, ddelta_bias=dbias)
+
+
+def _needs_grad(*ts):
+    return torch.is_grad_enabled() and any(
+        t is not None and isinstance(t, torch.Tensor) and t.requires_grad for t in ts)
 
 
 def lbm_selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None,
                        delta_softplus=True, window=None, reverse=False,
-                       return_last_state=False, discretize_mode="exp"):
+                       return_last_state=False, discretize_mode="exp", lb=True):
     """The north-star fused operator (LB scan).  Differentiable when any input
-    requires grad (backward = lbs_scan_bwd)."""
-    needs_grad = torch.is_grad_enabled() and any(
-        t is not None and isinstance(t, torch.Tensor) and t.requires_grad
-        for t in (u, delta, A, B, C, D, z, delta_bias))
-    if needs_grad:
-        from .autograd import LbmSelectiveScanFn
-        out = LbmSelectiveScanFn.apply(u, delta, A, B, C, D, z, delta_bias, delta_softplus,
-                                       window, reverse, True, discretize_mode)
+    requires grad (backward = lbs_scan_bwd, one fused launch + a reduction)."""
+    if _needs_grad(u, delta, A, B, C, D, z, delta_bias):
         if return_last_state:
-            raise NotImplementedError("return_last_state with autograd")
-        return out
+            raise NotImplementedError("return_last_state is not differentiable (the reference's "
+                                      "h_final has no adjoint either, autodiff.py:192-195)")
+        from .autograd import LbmSelectiveScanFn
+        return LbmSelectiveScanFn.apply(u, delta, A, B, C, D, z, delta_bias, delta_softplus,
+                                        window, reverse, lb, discretize_mode)
     return lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, window,
-                                  reverse, return_last_state, True, discretize_mode)
+                                  reverse, return_last_state, lb, discretize_mode)
 
 
 def selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_softplus=True,
                    reverse=False, return_last_state=False):
     """Plain unidirectional selective scan (engine.forward_scan_par semantics,
-    engine.py:294) — the same kernel with the LB pass compiled out."""
+    engine.py:294) — the same kernels with the LB pass compiled out."""
     # the window is irrelevant without the LB pass; 8-step tiles keep the
     # forward-only kernel on its fast full-tile path
-    return lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8,
-                                  reverse, return_last_state, False)
+    return lbm_selective_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8, reverse,
+                              return_last_state, "exp", lb=False)

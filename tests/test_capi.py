@@ -79,3 +79,51 @@ def test_python_api_rejects_cpu_tensors():
     x = torch.zeros(1, 4, 2)
     with pytest.raises(ShapeError):
         lbm_selective_scan(x, x, torch.zeros(2, 3), torch.zeros(1, 4, 3), torch.zeros(1, 4, 3))
+
+
+def test_long_window_is_rejected_not_hung():
+    """min(window, L) > 16 has no register tile: UNSUPPORTED, before any launch."""
+    L = _lib.lib()
+    rc = L.lbs_scan_fwd(C.byref(_args(seqlen=40, window=32)), None, 0, None)
+    assert rc == _lib.LBS_ERR_UNSUPPORTED
+    assert L.lbs_scan_fwd(C.byref(_args(seqlen=40, window=64)), None, 0, None) == _lib.LBS_ERR_UNSUPPORTED
+    with pytest.raises(NotImplementedError):
+        _lib.check(rc, "lbm_selective_scan")
+
+
+def test_checkpoint_plan():
+    L = _lib.lib()
+    # backward chunk = whole tiles in an 8-step (M <= 8) or 16-step register window
+    for M, K in ((1, 8), (3, 6), (4, 8), (5, 5), (8, 8), (9, 9), (16, 16)):
+        assert L.lbs_scan_ckpt_len(1000, M) == K
+    assert L.lbs_scan_ckpt_len(5, 16) == 5   # window clamps to L = 5
+    assert L.lbs_scan_ckpt_len(40, 32) == -1
+    a = _args(batch=2, seqlen=197, dim=384, dstate=16, window=8)
+    assert L.lbs_scan_ckpt_bytes(C.byref(a)) == 2 * 25 * 384 * 16 * 4
+    # a wrong ckpt_len is an argument error
+    a.checkpoints, a.ckpt_len = C.c_void_p(0x2000), 4
+    assert L.lbs_scan_fwd(C.byref(a), None, 0, None) == _lib.LBS_ERR_INVALID
+
+
+def _bwd_args(**kw):
+    a = _lib.ScanBwdArgs()
+    a.fwd = _args()
+    fake = C.c_void_p(0x3000)
+    for f in ("dout", "du", "ddelta", "dA", "dB", "dC"):
+        setattr(a, f, fake)
+    for k, v in kw.items():
+        setattr(a, k, v)
+    return a
+
+
+def test_bwd_argument_validation():
+    L = _lib.lib()
+    assert L.lbs_scan_bwd_workspace_bytes(C.byref(_bwd_args())) > 0
+    for kw, msg in ((dict(dout=None), "non-null"), (dict(dz=C.c_void_p(0x10)), "dz"),
+                    (dict(dD=C.c_void_p(0x10)), "dD")):
+        rc = L.lbs_scan_bwd(C.byref(_bwd_args(**kw)), None, 0, None)
+        assert rc == _lib.LBS_ERR_INVALID, kw
+        assert msg in L.lbs_last_error().decode()
+    # workspace is checked before any launch
+    assert L.lbs_scan_bwd(C.byref(_bwd_args()), None, 0, None) == _lib.LBS_ERR_INVALID
+    assert "workspace" in L.lbs_last_error().decode()
