@@ -192,3 +192,36 @@ def test_strided_views_like_the_block():
     g = lbm_selective_scan_bwd(dev(dout), **t, window=8)
     got = {k: (None if v is None else v.cpu().numpy()) for k, v in g.items()}
     check(got, O.lbm_selective_scan_bwd(dout, **inp, window=8), TOL_GRAD, "strided")
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_bwd_reproduces_reference_block_backward_golden(i):
+    """The GPU adjoint mapped onto the block's weights reproduces the UNMODIFIED
+    reference's block.block_backward (tests/golden/block.npz, made by
+    oracle/gen_golden.py) to the fp32-gradient bar — no oracle in between."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "block.npz"))
+    D, E, N, L, B, M, k, linear, rev, seed = [int(v) for v in g[f"b{i}_meta"]]
+    w = {f: g[f"b{i}_w_{f}"] for f in O.BLOCK_FIELDS}
+    mode = "linear" if linear else "exp"
+    T = g[f"b{i}_T"]
+    gout = g[f"b{i}_gout"]
+    if rev:
+        gout = gout[:, ::-1]
+    xs, z, x, xc = (g[f"b{i}_cache_{k}"] for k in ("xs", "z", "x", "xc"))
+    A = -np.exp(w["a_log"])
+    dout = gout @ w["w_out"].T
+    inp = dict(u=xs, delta=xs @ w["w_delta"], A=A, B=xs @ w["w_b"], C=xs @ w["w_c"], D=w["d_param"], z=z,
+               delta_bias=w["delta_bias"])
+    r = gpu_bwd(inp, dout, window=M, discretize_mode=mode)
+    r = {kk: (None if v is None else v.astype(np.float64)) for kk, v in r.items()}
+    xT = lambda a, b: np.tensordot(a, b, axes=((0, 1), (0, 1)))
+    xn = O.rms_norm(T, w["norm_scale"])
+    got = {"d_param": r["dD"], "delta_bias": r["ddelta_bias"], "a_log": r["dA"] * A,
+           "w_b": xT(xs, r["dB"]), "w_c": xT(xs, r["dC"]), "w_delta": xT(xs, r["ddelta"]),
+           "w_z": xT(xn, r["dz"])}
+    g_xs = r["du"] + r["ddelta"] @ w["w_delta"].T + r["dB"] @ w["w_b"].T + r["dC"] @ w["w_c"].T
+    _, got["conv_kernel"] = O.causal_conv1d_grad(x, w["conv_kernel"], g_xs * O.silu_grad(xc))
+    for name, v in got.items():
+        err = O.max_rel_err(v, g[f"b{i}_g_{name}"])
+        assert err <= TOL_GRAD, (name, err)

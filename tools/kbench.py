@@ -15,7 +15,7 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2506_15976_b200.scan import lbm_selective_scan_fwd  # noqa: E402
+from paper_2506_15976_b200.scan import lbm_selective_scan_bwd, lbm_selective_scan_fwd  # noqa: E402
 
 CFGS = {
     # name: (Bt, L, E, N, M, io dtype, bc dtype)
@@ -42,6 +42,13 @@ def alg_bytes(Bt, L, E, N, s_in, s_bc, s_out, last_state=False):
     if last_state:
         b += 4 * Bt * E * N
     return b
+
+
+def bwd_alg_bytes(Bt, L, E, N, s_in, s_bc, s_g):
+    # SURVEY §8d bwd: s_in*B*L*(3E+2N) + s_g*B*L*E (dout) + s_g*B*L*3E (du, ddelta, dz)
+    #                 + 4*B*L*2N (dB, dC fp32) + 4*(E*N + 2E)
+    return (s_in * Bt * L * 3 * E + s_bc * Bt * L * 2 * N + s_g * Bt * L * E + s_g * Bt * L * 3 * E
+            + 4 * Bt * L * 2 * N + 4 * (E * N + 2 * E))
 
 
 def make(Bt, L, E, N, io, bc, seed=0):
@@ -75,6 +82,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--only", default="")
+    ap.add_argument("--bwd", default="cfg1,cfg3", help="configs that also time the backward")
     a = ap.parse_args()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     peak = peak_gbs()
@@ -92,6 +100,18 @@ def main():
             print(json.dumps(dict(cfg=name, variant=variant, ms=round(ms, 4), gbs=round(gbs, 1),
                                   frac=round(gbs / peak, 3), elems_per_s=Bt * L * E / ms * 1e3,
                                   lanes_per_s=Bt * L * E * N / ms * 1e3)), flush=True)
+        if a.bwd and name in a.bwd.split(","):
+            dout = torch.randn(Bt, L, E, device="cuda").to(io)
+            _, ck = lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True)
+            nb = bwd_alg_bytes(Bt, L, E, N, s, sbc, s)
+            for variant, kw in (("bwd_ckpt", dict(checkpoints=ck)), ("bwd_recompute", {})):
+                ms = time_fn(lambda: lbm_selective_scan_bwd(dout, **x, window=M, **kw), a.iters, flush)
+                gbs = nb / ms / 1e6
+                print(json.dumps(dict(cfg=name, variant=variant, ms=round(ms, 4), gbs=round(gbs, 1),
+                                      frac=round(gbs / peak, 3), lanes_per_s=Bt * L * E * N / ms * 1e3)),
+                      flush=True)
+            ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True), a.iters, flush)
+            print(json.dumps(dict(cfg=name, variant="lbm_fwd_with_ckpt", ms=round(ms, 4))), flush=True)
 
 
 if __name__ == "__main__":
