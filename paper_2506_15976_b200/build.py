@@ -41,9 +41,9 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+def _compile(src: str, verbose: bool, objdir: str = OBJ, defines=()) -> str:
+    obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -70,9 +70,30 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Dev experiments: the whole library with extra -D flags into
+    variants/<name>.so (load it via LBSCAN_B200_LIB; travels with gpurun)."""
+    objdir = os.path.join(OBJ, "variants", name)
+    os.makedirs(objdir, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    with cf.ThreadPoolExecutor(max_workers=8) as ex:
+        objs = list(ex.map(lambda s: _compile(s, False, objdir, defines), srcs))
+    os.makedirs(os.path.join(ROOT, "variants"), exist_ok=True)
+    lib = os.path.join(ROOT, "variants", f"{name}.so")
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return lib
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--variant", default=None, help="name of an experimental build (with --define)")
+    ap.add_argument("--define", action="append", default=[])
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    if a.variant:
+        print(build_variant(a.variant, a.define))
+    else:
+        print(build(force=a.force, verbose=a.verbose))

@@ -58,13 +58,15 @@ struct FwdCfg {
 //   seq[2 stages][3 arrays][CL][128]  (Tio)   u, delta, z
 //   bcf[CL][2*NS]                      (f32)   B then C per step, zero padded
 //   a2s[NS/2][128]                     (f2)    A*log2(e) per channel pair
-template <typename Tio, int NS>
+//   bcraw[2 stages][CL][2*NS]           (Tbc)   B|C rows as loaded (cp.async path)
+template <typename Tio, typename Tbc, int NS>
 struct FwdSmem {
   static constexpr int CL = FwdCfg<Tio>::CL;
   static constexpr size_t seq_bytes = 2ull * 3 * CL * kFwdThreads * sizeof(Tio);
   static constexpr size_t bc_bytes = (size_t)CL * 2 * NS * sizeof(float);
   static constexpr size_t a2_bytes = (size_t)(NS / 2) * kFwdThreads * sizeof(f2);
-  static constexpr size_t total = seq_bytes + bc_bytes + a2_bytes;
+  static constexpr size_t raw_bytes = 2ull * CL * 2 * NS * sizeof(Tbc);
+  static constexpr size_t total = seq_bytes + bc_bytes + a2_bytes + raw_bytes;
 };
 
 // Per-thread staging plan for u/delta/z rows.  With 16-byte pieces each
@@ -159,6 +161,64 @@ struct BcPrefetch {
   }
 };
 
+// B/C staging for one chunk.  kAsync (N == NS, rows of 16-byte pieces): the
+// raw rows are copied by cp.async into a 2-stage shared-memory ring together
+// with u/delta/z — a global load the compiler cannot sink to its use — and
+// converted to the fp32 broadcast table at publish.  Otherwise: BcPrefetch.
+template <typename Tbc, int NS, int CL, bool kAsync>
+struct BcStage {
+  static constexpr int EPB = 16 / sizeof(Tbc);   // elements per 16-byte piece
+  static constexpr int PB = NS / EPB;            // pieces per B (or C) row
+  BcPrefetch<Tbc, NS, CL> pre;
+  const Tbc* base[2];
+  long long step;
+  __device__ __forceinline__ void init(const FwdParams& p, int b) {
+    if constexpr (kAsync) {
+      const bool rev = p.flags & LBS_FLAG_REVERSE;
+      const View3D* v[2] = {&p.Bm, &p.Cm};
+#pragma unroll
+      for (int w = 0; w < 2; ++w)
+        base[w] = static_cast<const Tbc*>(v[w]->p) + (long long)b * v[w]->s0 +
+                  (rev ? (long long)(p.L - 1) * v[w]->s1 : 0);
+      step = rev ? -p.Bm.s1 : p.Bm.s1;  // kAsync requires equal B/C row strides
+    } else {
+      pre.init(p, b);
+    }
+  }
+  __device__ __forceinline__ void issue(Tbc* raw, int stg, int c, int clen) {
+    if constexpr (kAsync) {
+      static_assert(CL * 2 * PB <= kFwdThreads || (CL * 2 * PB) % kFwdThreads == 0, "piece split");
+#pragma unroll
+      for (int i0 = 0; i0 < CL * 2 * PB; i0 += kFwdThreads) {
+        const int i = i0 + threadIdx.x;
+        const int t = i / (2 * PB), r = i % (2 * PB);
+        const int w = r / PB, piece = r % PB;
+        if (i < CL * 2 * PB && t < clen)
+          cp_async16(raw + ((size_t)(stg * CL + t) * 2 * NS + w * NS + piece * EPB),
+                     base[w] + (long long)(c + t) * step + piece * EPB);
+      }
+    } else {
+      pre.load(c, clen);
+    }
+  }
+  __device__ __forceinline__ void publish(float* bcf, const Tbc* raw, int stg, int clen) {
+    if constexpr (kAsync) {
+#pragma unroll
+      for (int i0 = 0; i0 < CL * 2 * NS; i0 += kFwdThreads) {
+        const int i = i0 + threadIdx.x;
+        const int t = i / (2 * NS);
+        bcf[i] = t < clen ? to_f(raw[(size_t)stg * CL * 2 * NS + i]) : 0.f;
+      }
+    } else {
+      pre.publish(bcf);
+    }
+  }
+};
+
+#ifndef LBS_QTRICK
+#define LBS_QTRICK 0
+#endif
+
 // One LB tile of r steps at ring rows [t0, t0+r): all state pairs, then the
 // D-skip + gate + store.  For MT > 8 the injections b_j are recomputed in the
 // forward sweep instead of held (keeps the 16-step window under 168 regs).
@@ -211,6 +271,33 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
         return mul2(bc2(du[j]), Bv);
       }
     };
+#if LBS_QTRICK
+    if (kLB) {
+      // LB record as Q_i = r_i + b_i = a_i Q_{i+1} + b_i (Q = b at a tile end), so
+      // h_i + r_i = a_i h_{i-1} + Q_i: one FFMA2 per step on the right-to-left chain
+      // and none extra on the left-to-right one.  At tile ends Q = b, so h + r is the
+      // forward state bit for bit (test_engine.py:107-114).
+      f2 Q[MT];
+#pragma unroll
+      for (int j = MT - 1; j >= 0; --j) {
+        if (kFull ? (j == MT - 1) : (j == r - 1)) {
+          Q[j] = binj(j);
+        } else if (kFull || j < r - 1) {
+          Q[j] = fma2(a[j], Q[j < MT - 1 ? j + 1 : j], binj(j));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        if (kFull || j < r) {
+          const f2 hr = fma2(a[j], h[q], Q[j]);
+          h[q] = fma2(a[j], h[q], binj(j));
+          const f2 Cv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + NS + 2 * q]);
+          yacc[j] = fma2(Cv, hr, yacc[j]);
+        }
+      }
+      continue;
+    }
+#endif
     if (kLB) {
       // exclusive tile-local backward record: r_{end} = 0, r_i = a_i (r_{i+1} + b_{i+1})
       f2 s = mk2(0.f, 0.f);
@@ -248,15 +335,26 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
   }
 }
 
+#ifndef LBS_FWD_MINB
+#define LBS_FWD_MINB 4
+#endif
+#ifndef LBS_BC_ASYNC
+#define LBS_BC_ASYNC 1
+#endif
+#ifndef LBS_FWD_MINB16
+#define LBS_FWD_MINB16 2
+#endif
+
 template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec>
-__global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? 4 : 2)) fwd_kernel(FwdParams p) {
+__global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16)) fwd_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
   constexpr int CL = FwdCfg<Tio>::CL;
-  using Sm = FwdSmem<Tio, NS>;
+  using Sm = FwdSmem<Tio, Tbc, NS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
   f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
+  Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes);
 
   const int tid = threadIdx.x;
   const int e0 = blockIdx.x * kFwdThreads;
@@ -304,14 +402,14 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? 4 : 2)) fwd_kernel(Fwd
 
   SeqStager<Tio, kVec> stager;
   stager.init(p, b, e0, has_z);
-  BcPrefetch<Tbc, NS, CL> bcpre;
-  bcpre.init(p, b);
+  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC> bcs;
+  bcs.init(p, b);
   // prologue: chunk 0
   int c = seg_lo;
   int clen = min(CLm, seg_hi - c);
   stager.issue(seq, 0, c, clen);
+  bcs.issue(bcraw, 0, c, clen);
   cp_async_commit();
-  bcpre.load(c, clen);
 
   for (int k = 0; c < seg_hi; ++k) {
     const int stg = k & 1;
@@ -319,10 +417,10 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? 4 : 2)) fwd_kernel(Fwd
     const int clen_n = cn < seg_hi ? min(CLm, seg_hi - cn) : 0;
     cp_async_wait_all();
     __syncthreads();  // chunk k landed (all threads); compute of chunk k-1 done
-    bcpre.publish(bcf);
+    bcs.publish(bcf, bcraw, stg, clen);
     if (clen_n > 0) {
       stager.issue(seq, stg ^ 1, cn, clen_n);
-      bcpre.load(cn, clen_n);
+      bcs.issue(bcraw, stg ^ 1, cn, clen_n);
     }
     cp_async_commit();
     __syncthreads();  // bcf visible
@@ -367,11 +465,12 @@ template <typename Tio, typename Tbc, int NS, bool kVec>
 __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
   constexpr int CL = FwdCfg<Tio>::CL;
-  using Sm = FwdSmem<Tio, NS>;
+  using Sm = FwdSmem<Tio, Tbc, NS>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
   f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
+  Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes);
 
   const int tid = threadIdx.x;
   const int e0 = blockIdx.x * kFwdThreads;
@@ -402,23 +501,23 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
 
   SeqStager<Tio, kVec> stager;
   stager.init(p, b, e0, false);
-  BcPrefetch<Tbc, NS, CL> bcpre;
-  bcpre.init(p, b);
+  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC> bcs;
+  bcs.init(p, b);
   int c = seg_lo;
   int clen = min(CL, seg_hi - c);
   stager.issue(seq, 0, c, clen);
+  bcs.issue(bcraw, 0, c, clen);
   cp_async_commit();
-  bcpre.load(c, clen);
   for (int k = 0; c < seg_hi; ++k) {
     const int stg = k & 1;
     const int cn = c + clen;
     const int clen_n = cn < seg_hi ? min(CL, seg_hi - cn) : 0;
     cp_async_wait_all();
     __syncthreads();
-    bcpre.publish(bcf);
+    bcs.publish(bcf, bcraw, stg, clen);
     if (clen_n > 0) {
       stager.issue(seq, stg ^ 1, cn, clen_n);
-      bcpre.load(cn, clen_n);
+      bcs.issue(bcraw, stg ^ 1, cn, clen_n);
     }
     cp_async_commit();
     __syncthreads();
@@ -460,7 +559,7 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
 
 template <typename Tio, typename Tbc, int NS, int MT, bool kVec>
 inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
-  const size_t smem = FwdSmem<Tio, NS>::total;
+  const size_t smem = FwdSmem<Tio, Tbc, NS>::total;
   dim3 block(kFwdThreads);
   if (p.n_seg > 1) {
     auto k1 = segment_state_kernel<Tio, Tbc, NS, kVec>;
@@ -491,21 +590,25 @@ inline cudaError_t launch_fwd_n(const FwdParams& p, cudaStream_t st) {
 }
 
 // 16-byte cp.async staging needs 16-byte aligned rows of whole pieces
-template <typename Tio>
+// (and B/C rows of N elements as whole 16-byte pieces with equal row strides)
+inline bool view_vec_ok(const View3D& v, size_t es) {
+  if (!v.p) return true;
+  return v.s2 == 1 && (reinterpret_cast<uintptr_t>(v.p) % 16) == 0 && (v.s0 * es) % 16 == 0 &&
+         (v.s1 * es) % 16 == 0;
+}
+
+template <typename Tio, typename Tbc>
 static bool vec_ok(const FwdParams& p) {
-  const size_t es = sizeof(Tio);
+  const size_t es = sizeof(Tio), eb = sizeof(Tbc);
   const int epp = 16 / (int)es;
-  auto ok = [&](const View3D& v) {
-    if (!v.p) return true;
-    return v.s2 == 1 && (reinterpret_cast<uintptr_t>(v.p) % 16) == 0 && (v.s0 * es) % 16 == 0 &&
-           (v.s1 * es) % 16 == 0;
-  };
-  return p.E % epp == 0 && ok(p.u) && ok(p.delta) && ok(p.z);
+  const int NS = p.N <= 4 ? 4 : 16;
+  const bool bc = p.N == NS && view_vec_ok(p.Bm, eb) && view_vec_ok(p.Cm, eb) && p.Bm.s1 == p.Cm.s1;
+  return p.E % epp == 0 && view_vec_ok(p.u, es) && view_vec_ok(p.delta, es) && view_vec_ok(p.z, es) && bc;
 }
 
 template <typename Tio, typename Tbc>
 inline cudaError_t launch_fwd_v(const FwdParams& p, cudaStream_t st) {
-  return vec_ok<Tio>(p) ? launch_fwd_n<Tio, Tbc, true>(p, st) : launch_fwd_n<Tio, Tbc, false>(p, st);
+  return vec_ok<Tio, Tbc>(p) ? launch_fwd_n<Tio, Tbc, true>(p, st) : launch_fwd_n<Tio, Tbc, false>(p, st);
 }
 
 }  // namespace lbs
