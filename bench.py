@@ -190,6 +190,50 @@ def scan_alg_bytes(B, L, E, N, s_io, s_bc):
     return s_io * B * L * 3 * E + s_bc * B * L * 2 * N + s_io * B * L * E + 4 * (E * N + 2 * E)
 
 
+def measure_ops(peak, iters=10):
+    """Kernel-level numbers for every BASELINE config on this GPU (rank 0): fused
+    LB fwd, forward-only fwd (the LB/fwd cost ratio of the north star) and, for
+    configs[2], the backward with training checkpoints.  CUDA events on the
+    launching stream, L2 flushed between launches, median of ``iters``."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from kbench import CFGS, alg_bytes, bwd_alg_bytes, make, time_fn
+
+    from paper_2506_15976_b200.scan import lbm_selective_scan_bwd, lbm_selective_scan_fwd
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    names = {"cfg1": "configs[0] op fwd fp32 B=2 E=192 L=197", "cfg2": "configs[1] LBVim-Ti layer scan bf16 B=256 E=384",
+             "cfg3": "configs[2] LBVim-S scan fp32 B=128 E=768 fwd+bwd", "cfg4": "configs[3] LBVim-S 1024^2 layer scan bf16 "
+             "B=32 L=4096 E=768", "cfg5": "configs[4] MIL bag fp32 B=1 L=100k E=512 (1 GPU)",
+             "cfg5s": "configs[4] one 8-way channel shard (E=64)"}
+    res = {}
+    for name, (Bt, L, E, N, M, io, bc) in CFGS.items():
+        x = make(Bt, L, E, N, io, bc)
+        out = torch.empty(Bt, L, E, device="cuda", dtype=io)
+        s_io = torch.tensor([], dtype=io).element_size()
+        s_bc = torch.tensor([], dtype=bc).element_size()
+        nb = alg_bytes(Bt, L, E, N, s_io, s_bc, s_io)
+        lb_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, out=out), iters, flush)
+        fw_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, lb=False, out=out), iters, flush)
+        r = {"what": names[name], "window": M, "lbm_fwd_ms": lb_ms, "fwd_only_ms": fw_ms,
+             "lb_over_fwd": lb_ms / fw_ms, "bytes": nb, "gbs": nb / lb_ms / 1e6, "frac": nb / lb_ms / 1e6 / peak,
+             "lanes_per_s": Bt * L * E * N / lb_ms * 1e3}
+        if name == "cfg3":
+            dout = torch.randn(Bt, L, E, device="cuda").to(io)
+            _, ck = lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True)
+            nbb = bwd_alg_bytes(Bt, L, E, N, s_io, s_bc, s_io)
+            bw_ms = time_fn(lambda: lbm_selective_scan_bwd(dout, **x, window=M, checkpoints=ck), iters, flush)
+            fck_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True), iters, flush)
+            r.update({"bwd_ms": bw_ms, "bwd_bytes": nbb, "bwd_gbs": nbb / bw_ms / 1e6,
+                      "bwd_frac": nbb / bw_ms / 1e6 / peak, "fwd_with_ckpt_ms": fck_ms,
+                      "fwd_bwd_ms": fck_ms + bw_ms, "fwd_bwd_gbs": (nb + nbb) / (fck_ms + bw_ms) / 1e6})
+            del dout, ck
+        res[name] = r
+        del x, out
+    del flush
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -320,6 +364,12 @@ def run_ours(args, rank, world, local_rank):
     step_ms = dev_ms / args.steps
     scan_share = cfg.depth * scan_ms / step_ms
 
+    ops = None
+    if rank == 0 and not args.no_ops:
+        ops = measure_ops(peak)
+    if world > 1:
+        dist.barrier()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference_run(steps=2, warmup=1)
@@ -343,7 +393,8 @@ def run_ours(args, rank, world, local_rank):
                          "share_of_step": scan_share,
                          "note": "MUFU/issue-bound: 1 ex2 + ~3.5 packed FP32 ops per state-step (DESIGN.md)"},
             "cpu_baseline": cpu,
-            "gpu_launches": 2 * cfg.depth * args.steps,
+            "ops": ops,
+            "gpu_launches": 3 * cfg.depth * args.steps,  # rms_norm + conv1d+SiLU + fused scan per block
             "clocks": clk.summary(),
             "wall_s_timed_region": t_wall,
         }
@@ -359,6 +410,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=GLOBAL_BATCH_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ops", action="store_true", help="skip the per-config kernel table")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", 0))

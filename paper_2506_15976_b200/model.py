@@ -32,10 +32,10 @@ from dataclasses import dataclass, field
 import torch
 import torch.nn.functional as F
 
-from .conv import causal_conv1d_silu_fwd
+from .conv import causal_conv1d_silu, causal_conv1d_silu_fwd
 from .errors import ShapeError
 from .norm import rms_norm
-from .scan import lbm_selective_scan_fwd
+from .scan import lbm_selective_scan, lbm_selective_scan_fwd
 from .tiling import select_tile_len
 
 RMS_EPS = 1e-6  # nn.py:13
@@ -290,3 +290,77 @@ class LBVim:
 
         run.graph, run.static_in, run.static_out = graph, static_in, static_out
         return run
+
+
+# ---------------------------------------------------------------------------
+# training path (autograd through the fused kernels)
+
+
+def block_forward_train(T, w: dict, M: int, reverse: bool = False, discretize_mode: str = "exp",
+                        lb: bool = True, eps: float = RMS_EPS):
+    """Differentiable LBVim block (block.py:158-190 forward, block.py:193-220 backward)
+    on the fused kernels: conv1d+SiLU (lbs_causal_conv1d_fwd/bwd) and the LB scan
+    (lbs_scan_fwd with checkpoints / lbs_scan_bwd) carry their own adjoints;
+    RMSNorm and the projections are stock torch autograd.  ``w`` holds the
+    reference's weight names (BLOCK_FIELDS).  As in ``LBVim.block`` the output is
+    NOT reversed: ``reverse`` selects the scan direction (flip-on-load)."""
+    xn = T * torch.rsqrt(T.float().pow(2).mean(-1, keepdim=True) + eps).to(T.dtype) * w["norm_scale"]
+    x = xn @ w["w_x"]
+    z = xn @ w["w_z"]
+    xs = causal_conv1d_silu(x, w["conv_kernel"], reverse=reverse)
+    delta = xs @ w["w_delta"]
+    Bm = xs @ w["w_b"]
+    Cm = xs @ w["w_c"]
+    A = -torch.exp(w["a_log"].float())
+    yg = lbm_selective_scan(xs, delta, A, Bm, Cm, D=w["d_param"], z=z, delta_bias=w["delta_bias"],
+                            window=M, reverse=reverse, discretize_mode=discretize_mode, lb=lb)
+    return yg @ w["w_out"] + T
+
+
+class LBVimTrainer:
+    """LBVim training step on the fused kernels: forward with autograd, cross
+    entropy, backward (lbs_scan_bwd / lbs_causal_conv1d_bwd + cuBLAS), AdamW.
+    Mirrors autodiff.train_step (autodiff.py:293-314) for the GAP / class-token
+    heads; blocks alternate direction by flip-on-load as in ``LBVim``."""
+
+    def __init__(self, cfg: ModelConfig, params: dict, lr: float = 1e-3, weight_decay: float = 0.05):
+        self.cfg = cfg
+        self.M = cfg.resolved_tile_len
+        self.params = {k: v.detach().clone().float().requires_grad_(True) for k, v in params.items()}
+        self.opt = torch.optim.AdamW(self.params.values(), lr=lr, weight_decay=weight_decay)
+
+    def forward(self, images):
+        cfg, p = self.cfg, self.params
+        B = images.shape[0]
+        g, ps = cfg.image_size // cfg.patch_size, cfg.patch_size
+        x = images.float().reshape(B, g, ps, g, ps, cfg.in_channels).permute(0, 1, 3, 2, 4, 5)
+        tok = x.reshape(B, g * g, -1) @ p["patch_w"] + p["patch_b"]
+        ct = cfg.class_token
+        if ct == "head":
+            tok = torch.cat([p["cls"][0].expand(B, 1, -1), tok], 1)
+        elif ct == "middle":
+            mid = tok.shape[1] // 2
+            tok = torch.cat([tok[:, :mid], p["cls"][0].expand(B, 1, -1), tok[:, mid:]], 1)
+        elif ct == "double":
+            tok = torch.cat([p["cls"][0].expand(B, 1, -1), tok, p["cls"][1].expand(B, 1, -1)], 1)
+        tok = tok + p["pos"]
+        rev = cfg.reverse_between_blocks
+        for i in range(cfg.depth):
+            w = {f: p[f"blocks.{i}.{f}"] for f in BLOCK_FIELDS}
+            tok = block_forward_train(tok, w, self.M, reverse=rev and i % 2 == 1,
+                                      discretize_mode=cfg.discretize_mode, lb=cfg.scan_variant == "lbm")
+        if ct != "none":
+            pos = {"head": [0], "middle": [cfg.num_patches // 2], "double": [0, cfg.seq_len - 1]}[ct]
+            pooled = torch.stack([tok[:, q] for q in pos], 1).mean(1)
+        else:
+            pooled = tok.mean(1)
+        h1 = F.gelu(pooled @ p["head.mlp_w1"] + p["head.mlp_b1"], approximate="tanh")
+        return h1 @ p["head.mlp_w2"] + p["head.mlp_b2"]
+
+    def step(self, images, labels):
+        """One optimisation step; returns the loss tensor (no host sync)."""
+        self.opt.zero_grad(set_to_none=True)
+        loss = F.cross_entropy(self.forward(images), labels)
+        loss.backward()
+        self.opt.step()
+        return loss.detach()
