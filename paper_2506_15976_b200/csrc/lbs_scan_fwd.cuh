@@ -45,13 +45,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-template <typename Tio>
+#ifndef LBS_FWD_CL
+#define LBS_FWD_CL 16  // steps per staged chunk (raised to the tile length for long windows)
+#endif
+
+template <typename Tio, int CLv = LBS_FWD_CL>
 struct FwdCfg {
-  static constexpr int CL = 16;                                // max steps per chunk
+  static constexpr int CL = CLv;                               // max steps per chunk
   static constexpr int PPR = kFwdThreads * sizeof(Tio) / 16;  // 16-byte pieces per ring row
   static constexpr int EPP = 16 / sizeof(Tio);                // elements per piece
   static constexpr int RS = kFwdThreads / PPR;                 // ring rows covered per pass
-  static constexpr int KP = CL / RS;                           // pieces per thread per array
+  static constexpr int KP = (CL + RS - 1) / RS;                // pieces per thread per array
 };
 
 // Shared-memory layout (dynamic):
@@ -59,23 +63,24 @@ struct FwdCfg {
 //   bcf[CL][2*NS]                      (f32)   B then C per step, zero padded
 //   a2s[NS/2][128]                     (f2)    A*log2(e) per channel pair
 //   bcraw[2 stages][CL][2*NS]           (Tbc)   B|C rows as loaded (cp.async path)
-template <typename Tio, typename Tbc, int NS>
+template <typename Tio, typename Tbc, int NS, int CLv = LBS_FWD_CL>
 struct FwdSmem {
-  static constexpr int CL = FwdCfg<Tio>::CL;
+  static constexpr int CL = CLv;
   static constexpr size_t seq_bytes = 2ull * 3 * CL * kFwdThreads * sizeof(Tio);
   static constexpr size_t bc_bytes = (size_t)CL * 2 * NS * sizeof(float);
   static constexpr size_t a2_bytes = (size_t)(NS / 2) * kFwdThreads * sizeof(f2);
   static constexpr size_t raw_bytes = 2ull * CL * 2 * NS * sizeof(Tbc);
-  static constexpr size_t total = seq_bytes + bc_bytes + a2_bytes + raw_bytes;
+  static constexpr size_t hs_bytes = (size_t)(NS / 2) * kFwdThreads * sizeof(f2);  // state spill area
+  static constexpr size_t total = seq_bytes + bc_bytes + a2_bytes + raw_bytes + hs_bytes;
 };
 
 // Per-thread staging plan for u/delta/z rows.  With 16-byte pieces each
 // thread owns one fixed piece column and rows t = row0 + k*RS, so all index
 // math is hoisted out of the chunk loop; "logical step l" addresses
 // base + l*step (step < 0 for the reverse direction = flip-on-load).
-template <typename Tio, bool kVec>
+template <typename Tio, bool kVec, int CLv = LBS_FWD_CL>
 struct SeqStager {
-  using C = FwdCfg<Tio>;
+  using C = FwdCfg<Tio, CLv>;
   const Tio* base[3];
   long long step[3];
   int narr, row0, col;
@@ -92,15 +97,15 @@ struct SeqStager {
     }
     ok = e0 + col < p.E;
     const int ec = ok ? e0 + col : 0;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const View3D& v = a == 0 ? p.u : (a == 1 ? p.delta : p.z);
-      const long long s1 = v.s1;
+    auto setup = [&](int a, const View3D v) {
       base[a] = v.p ? static_cast<const Tio*>(v.p) + (long long)b * v.s0 + (long long)ec * v.s2 +
-                          (rev ? (long long)(p.L - 1) * s1 : 0)
+                          (rev ? (long long)(p.L - 1) * v.s1 : 0)
                     : nullptr;
-      step[a] = rev ? -s1 : s1;
-    }
+      step[a] = rev ? -v.s1 : v.s1;
+    };
+    setup(0, p.u);
+    setup(1, p.delta);
+    setup(2, p.z);
   }
   __device__ __forceinline__ void issue(Tio* seq, int stg, int c, int clen) const {
     if (!ok) return;
@@ -124,7 +129,16 @@ struct SeqStager {
 // B/C of one chunk: each thread owns one fixed (B|C, n) column and rows
 // t = row0 + k*RS; values are prefetched into registers one chunk ahead and
 // published to shared memory as fp32 (zero for n >= N).
-template <typename Tbc, int NS, int CL>
+#ifndef LBS_BC_IL
+#define LBS_BC_IL 1  // forward B/C table layout: [t][pair q][B0 B1 C0 C1] (one LDS.128 per pair-step)
+#endif
+// index of (step t, B|C = w, state n) in the fp32 broadcast table
+template <int NS, bool kIL>
+__host__ __device__ constexpr int bc_index(int t, int w, int n) {
+  return kIL ? t * 2 * NS + (n >> 1) * 4 + w * 2 + (n & 1) : t * 2 * NS + w * NS + n;
+}
+
+template <typename Tbc, int NS, int CL, bool kIL = false>
 struct BcPrefetch {
   static constexpr int W = 2 * NS;                  // values per step
   static constexpr int RS = kFwdThreads / W;        // rows per pass
@@ -140,10 +154,15 @@ struct BcPrefetch {
     row0 = threadIdx.x / W;
     const int which = kk / NS, n = kk % NS;
     ok = n < p.N;
-    const View3D& vw = which == 0 ? p.Bm : p.Cm;
-    base = static_cast<const Tbc*>(vw.p) + (long long)b * vw.s0 + (long long)(ok ? n : 0) * vw.s2 +
-           (rev ? (long long)(p.L - 1) * vw.s1 : 0);
-    step = rev ? -vw.s1 : vw.s1;
+    // select by value (a reference to a runtime-chosen kernel parameter would
+    // force a local-memory copy of the whole parameter block)
+    const void* vp = which == 0 ? p.Bm.p : p.Cm.p;
+    const long long s0 = which == 0 ? p.Bm.s0 : p.Cm.s0;
+    const long long s1 = which == 0 ? p.Bm.s1 : p.Cm.s1;
+    const long long s2 = which == 0 ? p.Bm.s2 : p.Cm.s2;
+    base = static_cast<const Tbc*>(vp) + (long long)b * s0 + (long long)(ok ? n : 0) * s2 +
+           (rev ? (long long)(p.L - 1) * s1 : 0);
+    step = rev ? -s1 : s1;
   }
   __device__ __forceinline__ void load(int c, int clen) {
 #pragma unroll
@@ -156,7 +175,7 @@ struct BcPrefetch {
 #pragma unroll
     for (int k = 0; k < BCR; ++k) {
       const int t = row0 + k * RS;
-      if (t < CL) bcf[t * W + kk] = v[k];
+      if (t < CL) bcf[bc_index<NS, kIL>(t, kk / NS, kk % NS)] = v[k];
     }
   }
 };
@@ -165,21 +184,18 @@ struct BcPrefetch {
 // raw rows are copied by cp.async into a 2-stage shared-memory ring together
 // with u/delta/z — a global load the compiler cannot sink to its use — and
 // converted to the fp32 broadcast table at publish.  Otherwise: BcPrefetch.
-template <typename Tbc, int NS, int CL, bool kAsync>
+template <typename Tbc, int NS, int CL, bool kAsync, bool kIL = false>
 struct BcStage {
   static constexpr int EPB = 16 / sizeof(Tbc);   // elements per 16-byte piece
   static constexpr int PB = NS / EPB;            // pieces per B (or C) row
-  BcPrefetch<Tbc, NS, CL> pre;
+  BcPrefetch<Tbc, NS, CL, kIL> pre;
   const Tbc* base[2];
   long long step;
   __device__ __forceinline__ void init(const FwdParams& p, int b) {
     if constexpr (kAsync) {
       const bool rev = p.flags & LBS_FLAG_REVERSE;
-      const View3D* v[2] = {&p.Bm, &p.Cm};
-#pragma unroll
-      for (int w = 0; w < 2; ++w)
-        base[w] = static_cast<const Tbc*>(v[w]->p) + (long long)b * v[w]->s0 +
-                  (rev ? (long long)(p.L - 1) * v[w]->s1 : 0);
+      base[0] = static_cast<const Tbc*>(p.Bm.p) + (long long)b * p.Bm.s0 + (rev ? (long long)(p.L - 1) * p.Bm.s1 : 0);
+      base[1] = static_cast<const Tbc*>(p.Cm.p) + (long long)b * p.Cm.s0 + (rev ? (long long)(p.L - 1) * p.Cm.s1 : 0);
       step = rev ? -p.Bm.s1 : p.Bm.s1;  // kAsync requires equal B/C row strides
     } else {
       pre.init(p, b);
@@ -195,7 +211,7 @@ struct BcStage {
         const int w = r / PB, piece = r % PB;
         if (i < CL * 2 * PB && t < clen)
           cp_async16(raw + ((size_t)(stg * CL + t) * 2 * NS + w * NS + piece * EPB),
-                     base[w] + (long long)(c + t) * step + piece * EPB);
+                     (w ? base[1] : base[0]) + (long long)(c + t) * step + piece * EPB);
       }
     } else {
       pre.load(c, clen);
@@ -206,8 +222,8 @@ struct BcStage {
 #pragma unroll
       for (int i0 = 0; i0 < CL * 2 * NS; i0 += kFwdThreads) {
         const int i = i0 + threadIdx.x;
-        const int t = i / (2 * NS);
-        bcf[i] = t < clen ? to_f(raw[(size_t)stg * CL * 2 * NS + i]) : 0.f;
+        const int t = i / (2 * NS), kk = i % (2 * NS);
+        bcf[bc_index<NS, kIL>(t, kk / NS, kk % NS)] = t < clen ? to_f(raw[(size_t)stg * CL * 2 * NS + i]) : 0.f;
       }
     } else {
       pre.publish(bcf);
@@ -230,13 +246,132 @@ struct TileOut {
   float Dv;
 };
 
-template <typename Tio, int NS, int MT, bool kLB, bool kFull>
+#ifndef LBS_DBG_NOEXP
+#define LBS_DBG_NOEXP 0
+#endif
+#ifndef LBS_DBG_NOSOFTPLUS
+#define LBS_DBG_NOSOFTPLUS 0
+#endif
+#ifndef LBS_DBG_NOSTORE
+#define LBS_DBG_NOSTORE 0
+#endif
+
+#ifndef LBS_QUNROLL
+#define LBS_QUNROLL 2  // state pairs per unrolled group in a full tile; 0 = all (state in registers)
+#endif
+
+// One state pair (n, n+1) through one tile: exps, tile-local record, forward
+// recurrence, accumulation of C (h + r) into the per-step outputs.
+#ifndef LBS_HOLDC
+#define LBS_HOLDC 1  // with the interleaved table: one LDS.128 per pair-step, C held in registers
+#endif
+
+template <int NS, int MT, bool kLB, bool kFull, bool kIL = LBS_BC_IL>
+__device__ __forceinline__ void pair_tile(f2& hq, const f2 A2, int q, const float (&dl)[MT], const float (&du)[MT],
+                                          f2 (&yacc)[MT], const float* bcf, int t0, int r, bool linear) {
+  constexpr bool kHoldB = MT <= 8;
+  constexpr bool kHoldC = kIL && kHoldB && LBS_HOLDC;
+  f2 a[MT], bb[kHoldB ? MT : 1], cc[kHoldC ? MT : 1];
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    const f2 x = mul2(bc2(dl[j]), A2);
+#if LBS_DBG_NOEXP  // ablation only: no MUFU for the state decays
+    a[j] = fma2(x, bc2(0.01f), bc2(0.9f));
+#else
+    a[j] = linear ? x : mk2(ex2(x.x), ex2(x.y));
+#endif
+    if constexpr (kHoldC) {
+      const float4 v = *reinterpret_cast<const float4*>(&bcf[bc_index<NS, true>(t0 + j, 0, 2 * q)]);
+      bb[j] = mul2(bc2(du[j]), mk2(v.x, v.y));
+      cc[j] = mk2(v.z, v.w);
+    } else if constexpr (kHoldB) {
+      const f2 Bv = *reinterpret_cast<const f2*>(&bcf[bc_index<NS, kIL>(t0 + j, 0, 2 * q)]);
+      bb[j] = mul2(bc2(du[j]), Bv);
+    }
+  }
+  auto binj = [&](int j) -> f2 {
+    if constexpr (kHoldB) {
+      return bb[j];
+    } else {
+      const f2 Bv = *reinterpret_cast<const f2*>(&bcf[bc_index<NS, kIL>(t0 + j, 0, 2 * q)]);
+      return mul2(bc2(du[j]), Bv);
+    }
+  };
+  auto cinj = [&](int j) -> f2 {
+    if constexpr (kHoldC) {
+      return cc[j];
+    } else {
+      return *reinterpret_cast<const f2*>(&bcf[bc_index<NS, kIL>(t0 + j, 1, 2 * q)]);
+    }
+  };
+#if LBS_QTRICK
+  if (kLB) {
+    // LB record as Q_i = r_i + b_i = a_i Q_{i+1} + b_i (Q = b at a tile end), so
+    // h_i + r_i = a_i h_{i-1} + Q_i: one FFMA2 per step on the right-to-left chain.
+    // At tile ends Q = b, so h + r is the forward state bit for bit.
+    f2 Q[MT];
+#pragma unroll
+    for (int j = MT - 1; j >= 0; --j) {
+      if (kFull ? (j == MT - 1) : (j == r - 1)) {
+        Q[j] = binj(j);
+      } else if (kFull || j < r - 1) {
+        Q[j] = fma2(a[j], Q[j < MT - 1 ? j + 1 : j], binj(j));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < MT; ++j) {
+      if (kFull || j < r) {
+        const f2 hr = fma2(a[j], hq, Q[j]);
+        hq = fma2(a[j], hq, binj(j));
+        yacc[j] = fma2(cinj(j), hr, yacc[j]);
+      }
+    }
+    return;
+  }
+#endif
+  if (kLB) {
+    // exclusive tile-local backward record: r_{end} = 0, r_i = a_i (r_{i+1} + b_{i+1})
+    f2 s = mk2(0.f, 0.f);
+#pragma unroll
+    for (int j = MT - 1; j >= 0; --j) {
+      if (kFull ? (j == MT - 1) : (j == r - 1)) {
+        s = binj(j);
+      } else if (kFull || j < r - 1) {
+        const f2 rr = mul2(a[j], s);
+        yacc[j] = fma2(cinj(j), rr, yacc[j]);
+        s = add2(rr, binj(j));
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    if (kFull || j < r) {
+      hq = fma2(a[j], hq, binj(j));
+      yacc[j] = fma2(cinj(j), hq, yacc[j]);
+    }
+  }
+}
+
+// Fixed-size state store of a thread: registers (QU == NP: every loop over q is
+// unrolled) or this thread's column of a shared-memory array [NP][128] (QU < NP:
+// the pair loop stays rolled, which keeps the kernel's code in the I-cache).
+template <int NP, bool kRegs>
+struct StateStore {
+  f2 r[kRegs ? NP : 1];
+  f2* s;
+  __device__ __forceinline__ f2 get(int q) const { return kRegs ? r[kRegs ? q : 0] : s[q * kFwdThreads + threadIdx.x]; }
+  __device__ __forceinline__ void set(int q, f2 v) {
+    if constexpr (kRegs) r[q] = v;
+    else s[q * kFwdThreads + threadIdx.x] = v;
+  }
+};
+
+template <typename Tio, int NS, int MT, bool kLB, bool kFull, int QU, bool kRegs>
 __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const Tio* sz,
-                                             const float* bcf, const f2* a2s, f2 (&h)[NS / 2],
+                                             const float* bcf, const f2* a2s, StateStore<NS / 2, kRegs>& h,
                                              int t0, int r, float bias, bool softplus, bool linear,
                                              const TileOut& o) {
   constexpr int NP = NS / 2;
-  constexpr bool kHoldB = MT <= 8;
   const int tid = threadIdx.x;
   float dl[MT], du[MT];
   f2 yacc[MT];
@@ -245,80 +380,26 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
     const bool on = kFull || j < r;
     float d = on ? to_f(sd[(t0 + j) * kFwdThreads + tid]) + bias : 0.f;
     const float uv = on ? to_f(su[(t0 + j) * kFwdThreads + tid]) : 0.f;
+#if !LBS_DBG_NOSOFTPLUS
     if (softplus) d = softplus_f(d);
+#endif
     dl[j] = d;
     du[j] = d * uv;
     yacc[j] = mk2(o.Dv * uv, 0.f);  // D-skip folded into the accumulator
   }
+  if constexpr (kRegs) {
 #pragma unroll
-  for (int q = 0; q < NP; ++q) {
-    const f2 A2 = a2s[q * kFwdThreads + tid];
-    f2 a[MT], bb[kHoldB ? MT : 1];
+    for (int q = 0; q < NP; ++q)
+      pair_tile<NS, MT, kLB, kFull>(h.r[q], a2s[q * kFwdThreads + tid], q, dl, du, yacc, bcf, t0, r, linear);
+  } else {
+#pragma unroll 1
+    for (int q0 = 0; q0 < NP; q0 += QU) {
 #pragma unroll
-    for (int j = 0; j < MT; ++j) {
-      const f2 x = mul2(bc2(dl[j]), A2);
-      a[j] = linear ? x : mk2(ex2(x.x), ex2(x.y));
-      if constexpr (kHoldB) {
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + 2 * q]);
-        bb[j] = mul2(bc2(du[j]), Bv);
-      }
-    }
-    auto binj = [&](int j) -> f2 {
-      if constexpr (kHoldB) {
-        return bb[j];
-      } else {
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + 2 * q]);
-        return mul2(bc2(du[j]), Bv);
-      }
-    };
-#if LBS_QTRICK
-    if (kLB) {
-      // LB record as Q_i = r_i + b_i = a_i Q_{i+1} + b_i (Q = b at a tile end), so
-      // h_i + r_i = a_i h_{i-1} + Q_i: one FFMA2 per step on the right-to-left chain
-      // and none extra on the left-to-right one.  At tile ends Q = b, so h + r is the
-      // forward state bit for bit (test_engine.py:107-114).
-      f2 Q[MT];
-#pragma unroll
-      for (int j = MT - 1; j >= 0; --j) {
-        if (kFull ? (j == MT - 1) : (j == r - 1)) {
-          Q[j] = binj(j);
-        } else if (kFull || j < r - 1) {
-          Q[j] = fma2(a[j], Q[j < MT - 1 ? j + 1 : j], binj(j));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < MT; ++j) {
-        if (kFull || j < r) {
-          const f2 hr = fma2(a[j], h[q], Q[j]);
-          h[q] = fma2(a[j], h[q], binj(j));
-          const f2 Cv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + NS + 2 * q]);
-          yacc[j] = fma2(Cv, hr, yacc[j]);
-        }
-      }
-      continue;
-    }
-#endif
-    if (kLB) {
-      // exclusive tile-local backward record: r_{end} = 0, r_i = a_i (r_{i+1} + b_{i+1})
-      f2 s = mk2(0.f, 0.f);
-#pragma unroll
-      for (int j = MT - 1; j >= 0; --j) {
-        if (kFull ? (j == MT - 1) : (j == r - 1)) {
-          s = binj(j);
-        } else if (kFull || j < r - 1) {
-          const f2 rr = mul2(a[j], s);
-          const f2 Cv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + NS + 2 * q]);
-          yacc[j] = fma2(Cv, rr, yacc[j]);
-          s = add2(rr, binj(j));
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < MT; ++j) {
-      if (kFull || j < r) {
-        h[q] = fma2(a[j], h[q], binj(j));
-        const f2 Cv = *reinterpret_cast<const f2*>(&bcf[(t0 + j) * 2 * NS + NS + 2 * q]);
-        yacc[j] = fma2(Cv, h[q], yacc[j]);
+      for (int qq = 0; qq < QU; ++qq) {
+        const int q = q0 + qq;
+        f2 hq = h.get(q);
+        pair_tile<NS, MT, kLB, kFull>(hq, a2s[q * kFwdThreads + tid], q, dl, du, yacc, bcf, t0, r, linear);
+        h.set(q, hq);
       }
     }
   }
@@ -328,12 +409,19 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
     for (int j = 0; j < MT; ++j) {
       if (kFull || j < r) {
         float y = yacc[j].x + yacc[j].y;
+#if LBS_DBG_NOSTORE  // ablation only
+        if (y == 1234.5f) st<Tio>(op + (long long)(o.c + t0 + j) * o.step, y);
+#else
         if (o.has_z) y *= silu_f(to_f(sz[(t0 + j) * kFwdThreads + tid]));
         st<Tio>(op + (long long)(o.c + t0 + j) * o.step, y);
+#endif
       }
     }
   }
 }
+
+// chunk length of the main kernel: LBS_FWD_CL, but at least one whole tile
+constexpr int fwd_chunk(int mt) { return mt > LBS_FWD_CL ? mt : LBS_FWD_CL; }
 
 #ifndef LBS_FWD_MINB
 #define LBS_FWD_MINB 4
@@ -348,13 +436,16 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec>
 __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16)) fwd_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
-  constexpr int CL = FwdCfg<Tio>::CL;
-  using Sm = FwdSmem<Tio, Tbc, NS>;
+  constexpr int CL = fwd_chunk(MT);
+  using Sm = FwdSmem<Tio, Tbc, NS, CL>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
   f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
   Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes);
+  f2* hsm = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes + Sm::raw_bytes);
+  constexpr int QU = LBS_QUNROLL == 0 ? NP : LBS_QUNROLL;
+  constexpr bool kRegs = QU >= NP;
 
   const int tid = threadIdx.x;
   const int e0 = blockIdx.x * kFwdThreads;
@@ -382,15 +473,16 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
   const float Dv = p.D ? p.D[ec] : 0.f;
   const float bias = p.bias ? p.bias[ec] : 0.f;
 
-  f2 h[NP];
+  StateStore<NP, kRegs> h;
+  h.s = hsm;
 #pragma unroll
-  for (int q = 0; q < NP; ++q) h[q] = mk2(0.f, 0.f);
+  for (int q = 0; q < NP; ++q) h.set(q, mk2(0.f, 0.f));
   if (seg > 0) {
     const float* agg = p.seg_agg;
     for (int s = 0; s < seg; ++s) {
       const f2* PH = reinterpret_cast<const f2*>(agg + ((((long long)b * p.n_seg + s) * p.E + ec) * (2 * NS)));
 #pragma unroll
-      for (int q = 0; q < NP; ++q) h[q] = fma2(PH[q], h[q], PH[NP + q]);
+      for (int q = 0; q < NP; ++q) h.set(q, fma2(PH[q], h.get(q), PH[NP + q]));
     }
   }
 
@@ -400,9 +492,9 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
                                    (rev ? (long long)(L - 1) * p.so1 : 0);
   const long long ostep = rev ? -p.so1 : p.so1;
 
-  SeqStager<Tio, kVec> stager;
+  SeqStager<Tio, kVec, CL> stager;
   stager.init(p, b, e0, has_z);
-  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC> bcs;
+  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL> bcs;
   bcs.init(p, b);
   // prologue: chunk 0
   int c = seg_lo;
@@ -437,12 +529,24 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
         f2* ck = reinterpret_cast<f2*>(p.ckpt) +
                  (((long long)b * p.n_ckpt + (c + t0) / p.ckpt_len) * NP) * p.E + e;
 #pragma unroll
-        for (int q = 0; q < NP; ++q) ck[(long long)q * p.E] = h[q];
+        for (int q = 0; q < NP; ++q) ck[(long long)q * p.E] = h.get(q);
       }
       if (r == MT)
-        tile_compute<Tio, NS, MT, kLB, true>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
-      else
-        tile_compute<Tio, NS, MT, kLB, false>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, true, QU, kRegs>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
+      else {
+        // ragged tile (at most once per segment): rolled pair loop on the smem state
+        StateStore<NP, false> hp;
+        hp.s = hsm;
+        if constexpr (kRegs) {
+#pragma unroll
+          for (int q = 0; q < NP; ++q) hp.set(q, h.get(q));
+        }
+        tile_compute<Tio, NS, MT, kLB, false, 1, false>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
+        if constexpr (kRegs) {
+#pragma unroll
+          for (int q = 0; q < NP; ++q) h.set(q, hp.get(q));
+        }
+      }
     }
     c = cn;
     clen = clen_n;
@@ -452,8 +556,9 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
     float* hs = p.last_state + ((long long)b * p.E + e) * N;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      if (2 * q < N) hs[2 * q] = h[q].x;
-      if (2 * q + 1 < N) hs[2 * q + 1] = h[q].y;
+      const f2 hv = h.get(q);
+      if (2 * q < N) hs[2 * q] = hv.x;
+      if (2 * q + 1 < N) hs[2 * q + 1] = hv.y;
     }
   }
 }
@@ -464,8 +569,8 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
 template <typename Tio, typename Tbc, int NS, bool kVec>
 __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
-  constexpr int CL = FwdCfg<Tio>::CL;
-  using Sm = FwdSmem<Tio, Tbc, NS>;
+  constexpr int CL = LBS_FWD_CL;
+  using Sm = FwdSmem<Tio, Tbc, NS, CL>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
@@ -501,7 +606,7 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
 
   SeqStager<Tio, kVec> stager;
   stager.init(p, b, e0, false);
-  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC> bcs;
+  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL> bcs;
   bcs.init(p, b);
   int c = seg_lo;
   int clen = min(CL, seg_hi - c);
@@ -532,7 +637,7 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
       for (int q = 0; q < NP; ++q) {
         const f2 x = mul2(bc2(dl), a2s[q * kFwdThreads + tid]);
         const f2 a = linear ? x : mk2(ex2(x.x), ex2(x.y));
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[t * 2 * NS + 2 * q]);
+        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[bc_index<NS, LBS_BC_IL>(t, 0, 2 * q)]);
         H[q] = fma2(a, H[q], mul2(bc2(du), Bv));
         if (linear) P[q] = mul2(P[q], a);
       }
@@ -559,13 +664,14 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
 
 template <typename Tio, typename Tbc, int NS, int MT, bool kVec>
 inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
-  const size_t smem = FwdSmem<Tio, Tbc, NS>::total;
+  const size_t smem = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT)>::total;
   dim3 block(kFwdThreads);
   if (p.n_seg > 1) {
+    const size_t smem1 = FwdSmem<Tio, Tbc, NS, LBS_FWD_CL>::total;
     auto k1 = segment_state_kernel<Tio, Tbc, NS, kVec>;
-    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     dim3 g1((p.E + kFwdThreads - 1) / kFwdThreads, p.Bt, p.n_seg - 1);
-    k1<<<g1, block, smem, st>>>(p);
+    k1<<<g1, block, smem1, st>>>(p);
   }
   dim3 grid((p.E + kFwdThreads - 1) / kFwdThreads, p.Bt, p.n_seg);
   auto k = (p.flags & LBS_FLAG_LB) ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec>

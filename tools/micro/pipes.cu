@@ -14,6 +14,10 @@ __device__ __forceinline__ float ex2(float x) { float r; asm volatile("ex2.appro
 
 template <int MODE, int NACC>
 __global__ void k(float* out, int iters, float s) {
+  __shared__ float2 sm[256];
+  if (threadIdx.x < 256) sm[threadIdx.x] = make_float2(threadIdx.x, 1.f);
+  __syncthreads();
+  float2 lacc = make_float2(0.f, 0.f);
   f2 acc[NACC];
   float e[NACC];
 #pragma unroll
@@ -28,11 +32,15 @@ __global__ void k(float* out, int iters, float s) {
       if (MODE == 3) { acc[i] = fma2(acc[i], m, c); acc[i] = fma2(acc[i], m, c); acc[i] = fma2(acc[i], m, c);
                        e[i] = ex2(e[i]); }                              // 3 FFMA2 : 1 EX2
       if (MODE == 4) { acc[i] = fma2(acc[i], m, c); e[i] = ex2(e[i]); }  // 1 FFMA2 : 1 EX2
+      if (MODE == 5) { e[i] = ex2(e[i]); float2 v = sm[(it * 8 + i) & 255]; lacc.x += v.x; lacc.y += v.y; }  // EX2 + broadcast LDS.64
+      if (MODE == 6) { float2 v = sm[(it * 8 + i) & 255]; lacc.x += v.x; lacc.y += v.y; }  // broadcast LDS.64 only
+      if (MODE == 7) { e[i] = ex2(e[i]); float2 v = sm[(it * 8 + i) & 255]; float2 w = sm[(it * 8 + i + 1) & 255]; lacc.x += v.x + w.x; lacc.y += v.y * w.y; }  // EX2 + 2 LDS
     }
   }
   float t = 0;
 #pragma unroll
   for (int i = 0; i < NACC; ++i) t += acc[i].x + acc[i].y + e[i];
+  t += lacc.x + lacc.y;
   out[blockIdx.x * blockDim.x + threadIdx.x] = t;
 }
 
@@ -57,7 +65,12 @@ void run(const char* name, int ops_per_iter_per_acc, int threads, int blocks_per
 }
 
 int main() {
-  for (int bps : {1, 2, 4}) {
+  for (int bps : {4}) {
+    run<5>("EX2+LDS.64 (2 instr)", 2, 256, bps);
+    run<6>("LDS.64 bcast (1 instr)", 1, 256, bps);
+    run<7>("EX2+2xLDS.64 (3 instr)", 3, 256, bps);
+  }
+  for (int bps : {1, 4}) {
     run<0>("FFMA2 (1 instr)", 1, 256, bps);
     run<1>("FFMA (1 instr)", 1, 256, bps);
     run<2>("MUFU.EX2 (1 instr)", 1, 256, bps);
