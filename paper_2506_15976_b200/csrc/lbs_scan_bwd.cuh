@@ -53,13 +53,15 @@ struct BwdSmem {
   static constexpr size_t ck_bytes = 2ull * NP * kBwdThreads * sizeof(f2);
   static constexpr size_t pq_bytes = (size_t)NP * kBwdThreads * sizeof(f2);  // a2s, mu, dA each
   static constexpr size_t red_bytes = 4ull * KT * 2 * NS * sizeof(float);
+  static constexpr size_t raw_bytes = 2ull * KT * 2 * NS * 4;  // B|C rows as loaded (<= fp32)
   static constexpr size_t off_bc = seq_bytes;
   static constexpr size_t off_ck = off_bc + bc_bytes;
   static constexpr size_t off_a2 = off_ck + ck_bytes;
   static constexpr size_t off_mu = off_a2 + pq_bytes;
   static constexpr size_t off_da = off_mu + pq_bytes;
   static constexpr size_t off_red = off_da + pq_bytes;
-  static constexpr size_t total = off_red + red_bytes;
+  static constexpr size_t off_raw = off_red + red_bytes;
+  static constexpr size_t total = off_raw + raw_bytes;
 };
 
 // u / delta / z / dout rows of one chunk -> ring stage (see SeqStager).
@@ -73,7 +75,7 @@ struct BwdStager {
   long long step[4];
   int row0, col;
   bool ok;
-  __device__ __forceinline__ void init(const View3D* const* v, int L, bool rev, int b, int e0, int E) {
+  __device__ __forceinline__ void init(const View3D (&v)[4], int L, bool rev, int b, int e0, int E) {
     if constexpr (kVec) {
       row0 = threadIdx.x / PPR;
       col = (threadIdx.x % PPR) * EPP;
@@ -85,7 +87,7 @@ struct BwdStager {
     const int ec = ok ? e0 + col : 0;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      const View3D& w = *v[a];
+      const View3D w = v[a];
       base[a] = w.p ? static_cast<const Tio*>(w.p) + (long long)b * w.s0 + (long long)ec * w.s2 +
                           (rev ? (long long)(L - 1) * w.s1 : 0)
                     : nullptr;
@@ -151,7 +153,7 @@ struct BwdChunkCtx {
   float Dv, bias;
 };
 
-template <typename Tio, int NS, int KT, bool kLB, bool kFull>
+template <typename Tio, int NS, int KT, bool kLB, bool kFull, bool kOneTile>
 __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx& x, const Tio* su,
                                           const Tio* sd, const Tio* sz, const Tio* sg,
                                           const float* bcf, const f2* ck, const f2* a2s, f2* mu,
@@ -180,26 +182,33 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
   }
   const int jlast = kFull ? KT - 1 : clen - 1;
 
+  // tile boundaries: compile-time when the chunk is exactly one tile (M == KT, the
+  // LBVim / cfg-3 case), else the per-chunk masks
+  auto is_start = [&](int j) -> bool { return kOneTile ? j == 0 : (j == 0 || ((x.tstart >> j) & 1u)); };
+  auto is_end = [&](int j) -> bool {
+    return kOneTile ? (kFull ? j == KT - 1 : j == clen - 1) : ((x.tend >> j) & 1u);
+  };
 #pragma unroll 1
   for (int q = 0; q < NP; ++q) {
     const f2 A2 = a2s[q * kBwdThreads + tid];
     const f2 h0 = ck[q * kBwdThreads + tid];
     const f2 mu_in = mu[q * kBwdThreads + tid];
+    const float* bq = bcf + 4 * q;  // interleaved table: [t][q][B0 B1 C0 C1]
+    auto BC = [&](int j) -> float4 { return *reinterpret_cast<const float4*>(bq + j * 2 * NS); };
     f2 a[KT], h[KT], v[KT];
     // ---- ascending: a, h (state recompute from the checkpoint), LB adjoint v
     f2 hp = h0;
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
       if (kFull || j < clen) {
+        const float4 bc = BC(j);
         const f2 xa = mul2(bc2(dl[j]), A2);
         a[j] = x.linear ? xa : mk2(ex2(xa.x), ex2(xa.y));
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + 2 * q]);
-        hp = fma2(a[j], hp, mul2(bc2(dlu[j]), Bv));
+        hp = fma2(a[j], hp, mul2(bc2(dlu[j]), mk2(bc.x, bc.y)));
         h[j] = hp;
         if (kLB) {
-          const f2 Cv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + NS + 2 * q]);
-          const f2 g = mul2(bc2(gy[j]), Cv);
-          v[j] = (j == 0 || ((x.tstart >> j) & 1u)) ? g : fma2(a[j > 0 ? j - 1 : 0], v[j > 0 ? j - 1 : 0], g);
+          const f2 g = mul2(bc2(gy[j]), mk2(bc.z, bc.w));
+          v[j] = is_start(j) ? g : fma2(a[j > 0 ? j - 1 : 0], v[j > 0 ? j - 1 : 0], g);
         }
       } else {
         a[j] = mk2(0.f, 0.f);
@@ -214,12 +223,13 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
     for (int j = KT - 1; j >= 0; --j) {
       f2 dBv = mk2(0.f, 0.f), dCv = mk2(0.f, 0.f);
       if (kFull || j < clen) {
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + 2 * q]);
-        const f2 Cv = *reinterpret_cast<const f2*>(&bcf[j * 2 * NS + NS + 2 * q]);
+        const float4 bc = BC(j);
+        const f2 Bv = mk2(bc.x, bc.y);
+        const f2 Cv = mk2(bc.z, bc.w);
         const f2 bj = mul2(bc2(dlu[j]), Bv);
         const f2 g = mul2(bc2(gy[j]), Cv);
-        const bool tend = (x.tend >> j) & 1u;
-        const bool tstart = j == 0 || ((x.tstart >> j) & 1u);
+        const bool tend = is_end(j);
+        const bool tstart = is_start(j);
         f2 hr = h[j], Qc = bj;
         if (kLB && !tend) {
           hr = fma2(a[j], Qn, h[j]);
@@ -289,8 +299,12 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
   }
 }
 
+#ifndef LBS_BWD_MINB
+#define LBS_BWD_MINB 2
+#endif
+
 template <typename Tio, typename Tbc, int NS, int KT, bool kLB, bool kVec>
-__global__ void __launch_bounds__(kBwdThreads, 1) bwd_kernel(BwdParams P) {
+__global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParams P) {
   constexpr int NP = NS / 2;
   using Sm = BwdSmem<Tio, NS, KT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -301,6 +315,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_kernel(BwdParams P) {
   f2* mus = reinterpret_cast<f2*>(smem_raw + Sm::off_mu);
   f2* dAs = reinterpret_cast<f2*>(smem_raw + Sm::off_da);
   float* red = reinterpret_cast<float*>(smem_raw + Sm::off_red);
+  Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::off_raw);
 
   const FwdParams& p = P.f;
   const int tid = threadIdx.x;
@@ -347,11 +362,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_kernel(BwdParams P) {
   const long long sdz = rev ? -P.dz.s1 : P.dz.s1;
 
   const View3D zv = has_z ? p.z : View3D{nullptr, 0, 0, 0};
-  const View3D* views[4] = {&p.u, &p.delta, &zv, &P.dout};
+  const View3D views[4] = {p.u, p.delta, zv, P.dout};
   BwdStager<Tio, kVec, KT> stager;
   stager.init(views, L, rev, b, e0, p.E);
-  BcPrefetch<Tbc, NS, KT> bcpre;
-  bcpre.init(p, b);
+  BcStage<Tbc, NS, KT, kVec, true> bcs;  // interleaved fp32 table, cp.async when aligned
+  bcs.init(p, b);
+  const bool one_tile = m == KT;
   const f2* ckg = reinterpret_cast<const f2*>(p.ckpt) + (long long)b * nck * NP * p.E + ec;
   auto ck_issue = [&](int stg, int k) {
 #pragma unroll
@@ -364,18 +380,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_kernel(BwdParams P) {
   int clen = L - c;
   stager.issue(seq, 0, c, clen);
   ck_issue(0, k);
+  bcs.issue(bcraw, 0, c, clen);
   cp_async_commit();
-  bcpre.load(c, clen);
   const int eblk = blockIdx.x;
   for (int it = 0; k >= 0; ++it, --k) {
     const int stg = it & 1;
     cp_async_wait_all();
     __syncthreads();  // chunk k landed; chunk k+1 compute (and its partial write) done
-    bcpre.publish(bcf);
+    bcs.publish(bcf, bcraw, stg, clen);
     if (k > 0) {
       stager.issue(seq, stg ^ 1, c - K, K);
       ck_issue(stg ^ 1, k - 1);
-      bcpre.load(c - K, K);
+      bcs.issue(bcraw, stg ^ 1, c - K, K);
     }
     cp_async_commit();
     __syncthreads();  // bcf visible
@@ -400,12 +416,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1) bwd_kernel(BwdParams P) {
     const Tio* sz = base + 2 * KT * kBwdThreads;
     const Tio* sg = base + 3 * KT * kBwdThreads;
     const f2* ck = cks + stg * NP * kBwdThreads;
-    if (clen == KT)
-      bwd_chunk<Tio, NS, KT, kLB, true>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, dD_acc, dbias_acc,
-                                        dup, ddp, dzp, sdu, sdd, sdz);
-    else
-      bwd_chunk<Tio, NS, KT, kLB, false>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, dD_acc, dbias_acc,
-                                         dup, ddp, dzp, sdu, sdd, sdz);
+#define LBS_BWD_CHUNK(FULL, ONE)                                                                     \
+  bwd_chunk<Tio, NS, KT, kLB, FULL, ONE>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, dD_acc, dbias_acc, \
+                                         dup, ddp, dzp, sdu, sdd, sdz)
+    if (one_tile) {
+      if (clen == KT) LBS_BWD_CHUNK(true, true);
+      else LBS_BWD_CHUNK(false, true);
+    } else {
+      if (clen == KT) LBS_BWD_CHUNK(true, false);
+      else LBS_BWD_CHUNK(false, false);
+    }
+#undef LBS_BWD_CHUNK
     __syncthreads();  // red complete
     // dB / dC partials of this channel block: sum the 4 warps
     for (int i = tid; i < KT * 2 * NS; i += kBwdThreads) {
@@ -512,7 +533,10 @@ inline cudaError_t launch_bwd_v(const BwdParams& P, cudaStream_t st) {
     return v.s2 == 1 && (reinterpret_cast<uintptr_t>(v.p) % 16) == 0 && (v.s0 * es) % 16 == 0 &&
            (v.s1 * es) % 16 == 0;
   };
-  const bool vec = P.f.E % epp == 0 && ok(P.f.u) && ok(P.f.delta) && ok(P.f.z) && ok(P.dout);
+  const size_t eb = sizeof(Tbc);
+  const int NS = P.f.N <= 4 ? 4 : 16;
+  const bool bc = P.f.N == NS && view_vec_ok(P.f.Bm, eb) && view_vec_ok(P.f.Cm, eb) && P.f.Bm.s1 == P.f.Cm.s1;
+  const bool vec = P.f.E % epp == 0 && ok(P.f.u) && ok(P.f.delta) && ok(P.f.z) && ok(P.dout) && bc;
   return vec ? launch_bwd_n<Tio, Tbc, true>(P, st) : launch_bwd_n<Tio, Tbc, false>(P, st);
 }
 

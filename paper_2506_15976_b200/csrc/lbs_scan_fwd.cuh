@@ -223,7 +223,8 @@ struct BcStage {
       for (int i0 = 0; i0 < CL * 2 * NS; i0 += kFwdThreads) {
         const int i = i0 + threadIdx.x;
         const int t = i / (2 * NS), kk = i % (2 * NS);
-        bcf[bc_index<NS, kIL>(t, kk / NS, kk % NS)] = t < clen ? to_f(raw[(size_t)stg * CL * 2 * NS + i]) : 0.f;
+        if (i < CL * 2 * NS)  // (CL * 2 * NS may be < the 128 threads, e.g. N = 4 in the backward)
+          bcf[bc_index<NS, kIL>(t, kk / NS, kk % NS)] = t < clen ? to_f(raw[(size_t)stg * CL * 2 * NS + i]) : 0.f;
       }
     } else {
       pre.publish(bcf);

@@ -225,3 +225,18 @@ def test_bwd_reproduces_reference_block_backward_golden(i):
     for name, v in got.items():
         err = O.max_rel_err(v, g[f"b{i}_g_{name}"])
         assert err <= TOL_GRAD, (name, err)
+
+
+@pytest.mark.parametrize("N", [4, 16])
+@pytest.mark.parametrize("M", [3, 8])
+def test_bwd_vectorised_path_small_state(N, M):
+    """E multiple of 4 and 16-byte aligned rows -> the cp.async staging path;
+    N = 4 makes the B/C table smaller than the CTA (regression: out-of-table
+    writes clobbered the staged checkpoints)."""
+    inp, dout = case(19 + N + M, 2, 40, 16, N)
+    for ck in (False, True):
+        t = {k: dev(v) for k, v in inp.items()}
+        c = lbm_selective_scan_fwd(**t, window=M, save_checkpoints=True)[1] if ck else None
+        g = lbm_selective_scan_bwd(dev(dout), **t, window=M, checkpoints=c)
+        got = {k: (None if v is None else v.cpu().numpy()) for k, v in g.items()}
+        check(got, O.lbm_selective_scan_bwd(dout, **inp, window=M), TOL_GRAD, f"vec N={N} M={M} ck={ck}")

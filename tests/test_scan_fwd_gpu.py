@@ -259,3 +259,14 @@ def test_rms_norm(dtype, D):
     xq = dev(x, dtype).double().cpu().numpy()
     ref = O.rms_norm(xq, s)
     assert O.max_rel_err(got, ref) <= (TOL_F32 if dtype == torch.float32 else 1e-2)
+
+
+@pytest.mark.parametrize("N", [4, 8, 16])
+def test_fused_vectorised_path_state_sizes(N):
+    """E multiple of 8 (bf16) / 4 (fp32) with aligned rows -> cp.async staging path."""
+    inp = op_inputs(40 + N, 2, 99, 16, N)
+    for reverse in (False, True):
+        got, hf = run_gpu(inp, window=8, reverse=reverse, return_last_state=True)
+        ref, rhf = O.lbm_selective_scan(**inp, window=8, reverse=reverse, return_last_state=True)
+        assert O.max_rel_err(got, ref) <= TOL_F32
+        assert O.max_rel_err(hf, rhf) <= TOL_F32
