@@ -13,6 +13,7 @@
 // steps) keeps the K-1 step history in registers; a warp covers 32
 // consecutive channels, so every step is one contiguous row segment.
 #include <string>
+#include <type_traits>
 
 #include "lbs_common.cuh"
 #include "lbs_internal.h"
@@ -81,6 +82,165 @@ __global__ void __launch_bounds__(kConvThreads) conv_fwd_kernel(ConvParams p) {
 #pragma unroll
       for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
     }
+  }
+}
+
+// Vectorised forward: one thread = (b, CH-step chunk, V consecutive channels) with
+// V = 16 B / sizeof(T); 16-byte loads/stores of whole channel groups (a warp moves
+// 512 contiguous bytes per row), the K-1 step history in registers, GRP rows of
+// loads issued before use.  Requires E % V == 0, unit channel stride and 16-byte
+// aligned rows (checked by the launcher).
+#ifndef LBS_CONV_SMEM
+#define LBS_CONV_SMEM 1
+#endif
+#ifndef LBS_CONV_CHUNK
+#define LBS_CONV_CHUNK 16
+#endif
+#ifndef LBS_CONV_GRP
+#define LBS_CONV_GRP 16
+#endif
+constexpr int kConvVecChunk = LBS_CONV_CHUNK;
+
+template <typename T, int KW>
+__global__ void __launch_bounds__(kConvThreads) conv_fwd_vec_kernel(ConvParams p, int ngroups, int nchunks) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int GRP = LBS_CONV_GRP;
+  const long long idx = (long long)blockIdx.x * kConvThreads + threadIdx.x;
+  const int g = (int)(idx % ngroups);
+  const long long rest = idx / ngroups;
+  const int chunk = (int)(rest % nchunks);
+  const int b = (int)(rest / nchunks);
+  if (b >= p.Bt) return;
+  const int L = p.L, e0 = g * V;
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  float w[KW][V], bias[V];
+#pragma unroll
+  for (int c = 0; c < V; ++c) {
+#pragma unroll
+    for (int q = 0; q < KW; ++q) w[q][c] = q < p.K ? p.w[(long long)(e0 + c) * p.K + q] : 0.f;
+    bias[c] = p.bias ? p.bias[e0 + c] : 0.f;
+  }
+  const T* xp = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
+  T* op = static_cast<T*>(p.out) + (long long)b * p.so0 + e0;
+  auto phys = [&](int l) -> long long { return rev ? (L - 1 - l) : l; };
+  auto load_row = [&](int l, float (&r)[V]) {
+    if (l >= 0 && l < L) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(xp + phys(l) * p.x.s1);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int c = 0; c < V; ++c) r[c] = to_f(e[c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < V; ++c) r[c] = 0.f;
+    }
+  };
+  const int l0 = chunk * kConvVecChunk;
+  const int l1 = min(L, l0 + kConvVecChunk);
+  float hist[KW][V];  // hist[q] = x[l - q]
+#pragma unroll
+  for (int q = 1; q < KW; ++q) load_row(q < p.K ? l0 - q : -1, hist[q]);
+  for (int l = l0; l < l1; l += GRP) {
+    // GRP rows in flight, kept packed (4 registers each) until their step
+    uint4 raw[GRP];
+#pragma unroll
+    for (int i = 0; i < GRP; ++i)
+      raw[i] = (l + i < l1) ? *reinterpret_cast<const uint4*>(xp + phys(l + i) * p.x.s1) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < GRP; ++i) {
+#pragma unroll
+      for (int q = KW - 1; q >= 1; --q)
+#pragma unroll
+        for (int c = 0; c < V; ++c) hist[q][c] = hist[q - 1][c];
+      const T* xe = reinterpret_cast<const T*>(&raw[i]);
+#pragma unroll
+      for (int c = 0; c < V; ++c) hist[0][c] = to_f(xe[c]);
+      if (l + i < l1) {
+        uint4 raw;
+        T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+        for (int c = 0; c < V; ++c) {
+          float acc = bias[c];
+#pragma unroll
+          for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q][c], hist[q][c], acc);
+          const float y = act ? silu_f(acc) : acc;
+          if constexpr (sizeof(T) == 4) e[c] = y;
+          else if constexpr (std::is_same<T, __nv_bfloat16>::value) e[c] = __float2bfloat16_rn(y);
+          else e[c] = __float2half_rn(y);
+        }
+        *reinterpret_cast<uint4*>(op + phys(l + i) * p.so1) = raw;
+      }
+    }
+  }
+}
+
+// Shared-memory staged forward (the default when rows are 16-byte aligned): a
+// CTA owns (b, kConvTileT steps, kConvTileE channels).  Its (T + K - 1) input
+// rows are copied with cp.async 16-byte pieces — every load of the tile in
+// flight at once — then each thread sweeps one channel through the tile from
+// shared memory with the K-1 history in registers.  Flip-on-load: logical row l
+// is physical L-1-l.
+#ifndef LBS_CONV_TILE_T
+#define LBS_CONV_TILE_T 32
+#endif
+constexpr int kConvTileT = LBS_CONV_TILE_T;
+constexpr int kConvTileE = 256;
+
+__device__ __forceinline__ void cp_async16_conv(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+template <typename T, int KW>
+__global__ void __launch_bounds__(kConvTileE) conv_fwd_smem_kernel(ConvParams p) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int ROWS = kConvTileT + KW - 1;
+  __shared__ __align__(16) T tile[ROWS][kConvTileE];
+  const int e0 = blockIdx.x * kConvTileE;
+  const int l0 = blockIdx.y * kConvTileT;
+  const int b = blockIdx.z;
+  const int L = p.L;
+  const int EC = min(kConvTileE, p.E - e0);
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
+  // stage rows l0-(KW-1) .. l0+T-1 (logical); out-of-range rows are zero (causal pad)
+  const int pieces_per_row = EC / V;
+  for (int i = threadIdx.x; i < ROWS * pieces_per_row; i += kConvTileE) {
+    const int r = i / pieces_per_row, pc = i - r * pieces_per_row;
+    const int l = l0 - (KW - 1) + r;
+    T* dst = &tile[r][pc * V];
+    if (l >= 0 && l < L) {
+      const long long ph = rev ? (L - 1 - l) : l;
+      cp_async16_conv(dst, xb + ph * p.x.s1 + pc * V);
+    } else {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c >= EC) return;
+  const int e = e0 + c;
+  float w[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) w[q] = q < p.K ? p.w[(long long)e * p.K + q] : 0.f;
+  const float bias = p.bias ? p.bias[e] : 0.f;
+  float hist[KW];  // hist[q] = x[l - q]
+#pragma unroll
+  for (int q = 1; q < KW; ++q) hist[q] = to_f(tile[KW - 1 - q][c]);
+  T* ob = static_cast<T*>(p.out) + (long long)b * p.so0 + (long long)e * p.so2;
+  const int T_ = min(kConvTileT, L - l0);
+#pragma unroll 4
+  for (int j = 0; j < T_; ++j) {
+    hist[0] = to_f(tile[KW - 1 + j][c]);
+    float acc = bias;
+#pragma unroll
+    for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], hist[q], acc);
+    const int l = l0 + j;
+    st<T>(ob + (long long)(rev ? (L - 1 - l) : l) * p.so1, act ? silu_f(acc) : acc);
+#pragma unroll
+    for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
   }
 }
 
@@ -163,7 +323,31 @@ __global__ void conv_reduce_kernel(const float* part, int n_part, int E, int K, 
 }
 
 template <typename T>
+static bool conv_vec_ok(const ConvParams& p) {
+  constexpr int V = 16 / sizeof(T);
+  auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+  return p.E % V == 0 && p.x.s2 == 1 && p.so2 == 1 && al(p.x.p) && al(p.out) && p.x.s0 % V == 0 &&
+         p.x.s1 % V == 0 && p.so0 % V == 0 && p.so1 % V == 0;
+}
+
+template <typename T>
 static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
+  if (conv_vec_ok<T>(p) && LBS_CONV_SMEM) {
+    dim3 grid((p.E + kConvTileE - 1) / kConvTileE, (p.L + kConvTileT - 1) / kConvTileT, p.Bt);
+    if (p.K <= 4) conv_fwd_smem_kernel<T, 4><<<grid, kConvTileE, 0, st>>>(p);
+    else conv_fwd_smem_kernel<T, kMaxWidth><<<grid, kConvTileE, 0, st>>>(p);
+    return cudaGetLastError();
+  }
+  if (conv_vec_ok<T>(p)) {
+    constexpr int V = 16 / sizeof(T);
+    const int ngroups = p.E / V;
+    const int nchunks = (p.L + kConvVecChunk - 1) / kConvVecChunk;
+    const long long units = (long long)p.Bt * nchunks * ngroups;
+    const unsigned blocks = (unsigned)((units + kConvThreads - 1) / kConvThreads);
+    if (p.K <= 4) conv_fwd_vec_kernel<T, 4><<<blocks, kConvThreads, 0, st>>>(p, ngroups, nchunks);
+    else conv_fwd_vec_kernel<T, kMaxWidth><<<blocks, kConvThreads, 0, st>>>(p, ngroups, nchunks);
+    return cudaGetLastError();
+  }
   dim3 grid((p.E + kConvThreads - 1) / kConvThreads, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
   if (p.K <= 4) conv_fwd_kernel<T, 4><<<grid, kConvThreads, 0, st>>>(p);
   else conv_fwd_kernel<T, kMaxWidth><<<grid, kConvThreads, 0, st>>>(p);

@@ -6,47 +6,56 @@
 
 namespace lbs {
 
-template <typename T, int VPL>  // VPL = 16-byte vectors per lane (row <= 32*VPL*EPV)
+template <typename T, int VPL, int RPW>  // VPL = 16-byte vectors per lane; RPW rows per warp
 __global__ void __launch_bounds__(256) rms_norm_kernel(const T* __restrict__ x, const float* __restrict__ scale,
                                                        T* __restrict__ out, long long rows, int D, float eps,
                                                        long long sx, long long so) {
   constexpr int EPV = 16 / sizeof(T);
-  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const long long row0 = ((long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32) * RPW;
   const int lane = threadIdx.x % 32;
-  if (row >= rows) return;
-  const T* xr = x + row * sx;
-  T* orow = out + row * so;
-  float v[VPL][EPV];
-  float ss = 0.f;
+  if (row0 >= rows) return;
+  // all RPW rows' loads are in flight before the first reduction (memory-level parallelism)
+  uint4 raw[RPW][VPL];
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const int c0 = (lane + 32 * k) * EPV;
-    if (c0 < D) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(xr + c0);
-      const T* e = reinterpret_cast<const T*>(&raw);
+  for (int r = 0; r < RPW; ++r)
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int c0 = (lane + 32 * k) * EPV;
+      if (row0 + r < rows && c0 < D) raw[r][k] = *reinterpret_cast<const uint4*>(x + (row0 + r) * sx + c0);
+      else raw[r][k] = make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    if (row0 + r >= rows) break;
+    float v[VPL][EPV];
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const T* e = reinterpret_cast<const T*>(&raw[r][k]);
 #pragma unroll
       for (int i = 0; i < EPV; ++i) {
         v[k][i] = to_f(e[i]);
         ss = fmaf(v[k][i], v[k][i], ss);
       }
     }
-  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float inv = rsqrtf(ss / (float)D + eps);
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = rsqrtf(ss / (float)D + eps);
+    T* orow = out + (row0 + r) * so;
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const int c0 = (lane + 32 * k) * EPV;
-    if (c0 < D) {
-      uint4 raw;
-      T* e = reinterpret_cast<T*>(&raw);
+    for (int k = 0; k < VPL; ++k) {
+      const int c0 = (lane + 32 * k) * EPV;
+      if (c0 < D) {
+        uint4 o4;
+        T* e = reinterpret_cast<T*>(&o4);
 #pragma unroll
-      for (int i = 0; i < EPV; ++i) {
-        float y = v[k][i] * inv * scale[c0 + i];
-        if constexpr (sizeof(T) == 4) e[i] = y;
-        else e[i] = __float2bfloat16_rn(y);
+        for (int i = 0; i < EPV; ++i) {
+          const float y = v[k][i] * inv * __ldg(scale + c0 + i);
+          if constexpr (sizeof(T) == 4) e[i] = y;
+          else e[i] = __float2bfloat16_rn(y);
+        }
+        *reinterpret_cast<uint4*>(orow + c0) = o4;
       }
-      *reinterpret_cast<uint4*>(orow + c0) = raw;
     }
   }
 }
@@ -84,9 +93,14 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
     rms_norm_scalar_kernel<T><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
     return cudaGetLastError();
   }
-  if (vpl <= 1) rms_norm_kernel<T, 1><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
-  else if (vpl <= 2) rms_norm_kernel<T, 2><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
-  else if (vpl <= 4) rms_norm_kernel<T, 4><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+#ifndef LBS_NORM_RPW
+#define LBS_NORM_RPW 1
+#endif
+  constexpr int RPW = LBS_NORM_RPW;
+  dim3 gridv((unsigned)((p.rows + 8 * RPW - 1) / (8 * RPW)));
+  if (vpl <= 1) rms_norm_kernel<T, 1, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+  else if (vpl <= 2) rms_norm_kernel<T, 2, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+  else if (vpl <= 4) rms_norm_kernel<T, 4, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }

@@ -238,6 +238,26 @@ def test_conv_fwd_bwd(reverse, K):
     assert O.max_rel_err(dw.cpu().numpy(), gw_ref) <= TOL_F32
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("K", [2, 4, 6])
+@pytest.mark.parametrize("reverse", [False, True])
+def test_conv_fwd_vectorised(dtype, K, reverse):
+    """16-byte channel-group path (E % 8 == 0, aligned rows), input a column view of
+    a wider projection output like the block's x = xz[..., :E]; L spans several
+    64-step chunks plus a ragged one."""
+    from paper_2506_15976_b200.conv import causal_conv1d_silu_fwd
+    rng = O.seeded_rng(K + 7 * reverse)
+    Bt, L, E = 3, 150, 64
+    xz = dev(rng.standard_normal((Bt, L, 2 * E)), dtype)
+    x = xz[..., :E]
+    w = rng.standard_normal((E, K)) * 0.5
+    xq = x.double().cpu().numpy()
+    flip = (lambda a: a[:, ::-1]) if reverse else (lambda a: a)
+    ref = flip(O.silu(O.causal_conv1d(flip(xq), w)))
+    got = causal_conv1d_silu_fwd(x, dev(w), reverse=reverse).float().cpu().numpy()
+    assert O.max_rel_err(got, ref) <= (TOL_F32 if dtype == torch.float32 else 1e-2)
+
+
 def test_conv_golden():
     from paper_2506_15976_b200.conv import causal_conv1d_silu_bwd, causal_conv1d_silu_fwd
     g = np.load(os.path.join(GOLD, "conv.npz"))
@@ -249,11 +269,12 @@ def test_conv_golden():
 
 
 @pytest.mark.parametrize("dtype,D", [(torch.float32, 192), (torch.bfloat16, 192), (torch.bfloat16, 384),
-                                     (torch.float32, 8)])
-def test_rms_norm(dtype, D):
+                                     (torch.float32, 8), (torch.bfloat16, 1024)])
+@pytest.mark.parametrize("rows", [1, 3 * 37, 4 * 64 + 3])
+def test_rms_norm(dtype, D, rows):
     from paper_2506_15976_b200.norm import rms_norm
-    rng = O.seeded_rng(D)
-    x = rng.standard_normal((3, 37, D))
+    rng = O.seeded_rng(D + rows)
+    x = rng.standard_normal((1, rows, D))
     s = rng.uniform(0.5, 1.5, D)
     got = rms_norm(dev(x, dtype), dev(s)).float().cpu().numpy()
     xq = dev(x, dtype).double().cpu().numpy()

@@ -1,4 +1,5 @@
-"""One eager LBVim-Ti forward at batch 256 bf16 (target for an ncu launch list)."""
+"""One eager LBVim-Ti forward at batch 256 bf16 inside a cudaProfilerStart/Stop
+range (target for an ncu launch list: ncu --profile-from-start off ...)."""
 import os
 import sys
 
@@ -13,4 +14,8 @@ x = torch.randn(int(os.environ.get("BATCH", 256)), 224, 224, 3, device="cuda").t
 for _ in range(int(os.environ.get("ITERS", 2))):
     net(x)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
+net(x)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("done")
