@@ -353,6 +353,48 @@ __device__ __forceinline__ void pair_tile(f2& hq, const f2 A2, int q, const floa
   }
 }
 
+#ifndef LBS_PIPE
+#define LBS_PIPE 0  // software-pipeline the state-pair loop: next pair's EX2s under this pair's chains
+#endif
+
+// Software-pipelined pieces of pair_tile for full tiles with MT <= 8: the
+// decays of pair q+1 (MUFU) are issued while the dependent FFMA2 chains of
+// pair q run, so one warp feeds both pipes (the plain loop issues them in turns).
+template <int NS, int MT>
+__device__ __forceinline__ void pair_exps(f2 (&a)[MT], const f2 A2, const float (&dl)[MT], bool linear) {
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    const f2 x = mul2(bc2(dl[j]), A2);
+    a[j] = linear ? x : mk2(ex2(x.x), ex2(x.y));
+  }
+}
+
+template <int NS, int MT, bool kLB>
+__device__ __forceinline__ void pair_chains(f2& hq, const f2 (&a)[MT], int q, const float (&du)[MT],
+                                            f2 (&yacc)[MT], const float* bcf, int t0) {
+  f2 bb[MT], cc[MT];
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    const float4 v = *reinterpret_cast<const float4*>(&bcf[bc_index<NS, true>(t0 + j, 0, 2 * q)]);
+    bb[j] = mul2(bc2(du[j]), mk2(v.x, v.y));
+    cc[j] = mk2(v.z, v.w);
+  }
+  if (kLB) {
+    f2 s = bb[MT - 1];
+#pragma unroll
+    for (int j = MT - 2; j >= 0; --j) {
+      const f2 rr = mul2(a[j], s);
+      yacc[j] = fma2(cc[j], rr, yacc[j]);
+      s = add2(rr, bb[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    hq = fma2(a[j], hq, bb[j]);
+    yacc[j] = fma2(cc[j], hq, yacc[j]);
+  }
+}
+
 // Fixed-size state store of a thread: registers (QU == NP: every loop over q is
 // unrolled) or this thread's column of a shared-memory array [NP][128] (QU < NP:
 // the pair loop stays rolled, which keeps the kernel's code in the I-cache).
@@ -392,6 +434,25 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 #pragma unroll
     for (int q = 0; q < NP; ++q)
       pair_tile<NS, MT, kLB, kFull>(h.r[q], a2s[q * kFwdThreads + tid], q, dl, du, yacc, bcf, t0, r, linear);
+  } else if constexpr (LBS_PIPE && kFull && MT <= 8 && LBS_BC_IL && NP % 2 == 0) {
+    // two-stage pipeline over state pairs, unrolled by 2 so the buffers swap names
+    f2 aA[MT], aB[MT];
+    pair_exps<NS, MT>(aA, a2s[tid], dl, linear);
+#pragma unroll 1
+    for (int q = 0; q < NP; q += 2) {
+      pair_exps<NS, MT>(aB, a2s[(q + 1) * kFwdThreads + tid], dl, linear);
+      {
+        f2 hq = h.get(q);
+        pair_chains<NS, MT, kLB>(hq, aA, q, du, yacc, bcf, t0);
+        h.set(q, hq);
+      }
+      if (q + 2 < NP) pair_exps<NS, MT>(aA, a2s[(q + 2) * kFwdThreads + tid], dl, linear);
+      {
+        f2 hq = h.get(q + 1);
+        pair_chains<NS, MT, kLB>(hq, aB, q + 1, du, yacc, bcf, t0);
+        h.set(q + 1, hq);
+      }
+    }
   } else {
 #pragma unroll 1
     for (int q0 = 0; q0 < NP; q0 += QU) {
