@@ -214,7 +214,10 @@ def measure_ops(peak, iters=10):
         nb = alg_bytes(Bt, L, E, N, s_io, s_bc, s_io)
         lb_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, out=out), iters, flush)
         fw_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, lb=False, out=out), iters, flush)
+        from paper_2506_15976_b200.scan import global_bidir_selective_scan
+        bi_ms = time_fn(lambda: global_bidir_selective_scan(**x), iters, flush) if name in ("cfg2", "cfg4") else None
         r = {"what": names[name], "window": M, "lbm_fwd_ms": lb_ms, "fwd_only_ms": fw_ms,
+             "global_bidir_ms": bi_ms, "lb_over_bidir": (lb_ms / bi_ms) if bi_ms else None,
              "lb_over_fwd": lb_ms / fw_ms, "bytes": nb, "gbs": nb / lb_ms / 1e6, "frac": nb / lb_ms / 1e6 / peak,
              "lanes_per_s": Bt * L * E * N / lb_ms * 1e3}
         if name == "cfg3":

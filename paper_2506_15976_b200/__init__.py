@@ -9,13 +9,14 @@ from .errors import NonFiniteError, ShapeError
 from .tiling import TilePlan, select_tile_len
 
 __all__ = ["ShapeError", "NonFiniteError", "TilePlan", "select_tile_len",
-           "lbm_selective_scan", "selective_scan"]
+           "lbm_selective_scan", "selective_scan", "global_bidir_selective_scan"]
 
 
 def __getattr__(name):
     # torch-dependent API is imported lazily so `import paper_2506_15976_b200`
     # stays cheap for the C-ABI tests
-    if name in ("lbm_selective_scan", "selective_scan", "lbm_selective_scan_fwd"):
+    if name in ("lbm_selective_scan", "selective_scan", "lbm_selective_scan_fwd", "lbm_selective_scan_bwd",
+                "global_bidir_selective_scan"):
         from . import scan
         return getattr(scan, name)
     raise AttributeError(name)

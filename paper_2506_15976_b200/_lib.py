@@ -22,6 +22,7 @@ FLAG_REVERSE = 1 << 0
 FLAG_SOFTPLUS = 1 << 1
 FLAG_LB = 1 << 2
 FLAG_LINEAR = 1 << 3
+FLAG_ACCUM = 1 << 5
 CONV_SILU = 1 << 4
 
 I64 = C.c_int64

@@ -245,6 +245,7 @@ struct TileOut {
   int c;
   bool active, has_z;
   float Dv;
+  bool accum;      // out += y (LBS_FLAG_ACCUM)
 };
 
 #ifndef LBS_DBG_NOEXP
@@ -257,6 +258,9 @@ struct TileOut {
 #define LBS_DBG_NOSTORE 0
 #endif
 
+#ifndef LBS_QUNROLL16
+#define LBS_QUNROLL16 2  // the same for 16-step tiles
+#endif
 #ifndef LBS_QUNROLL
 #define LBS_QUNROLL 2  // state pairs per unrolled group in a full tile; 0 = all (state in registers)
 #endif
@@ -475,7 +479,9 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
         if (y == 1234.5f) st<Tio>(op + (long long)(o.c + t0 + j) * o.step, y);
 #else
         if (o.has_z) y *= silu_f(to_f(sz[(t0 + j) * kFwdThreads + tid]));
-        st<Tio>(op + (long long)(o.c + t0 + j) * o.step, y);
+        Tio* dst = op + (long long)(o.c + t0 + j) * o.step;
+        if (o.accum) y += to_f(*dst);
+        st<Tio>(dst, y);
 #endif
       }
     }
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
   f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
   Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes);
   f2* hsm = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes + Sm::raw_bytes);
-  constexpr int QU = LBS_QUNROLL == 0 ? NP : LBS_QUNROLL;
+  constexpr int QU = MT > 8 ? LBS_QUNROLL16 : (LBS_QUNROLL == 0 ? NP : LBS_QUNROLL);
   constexpr bool kRegs = QU >= NP;
 
   const int tid = threadIdx.x;
@@ -582,7 +588,7 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
     const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * kFwdThreads;
     const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * kFwdThreads;
     const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * kFwdThreads;
-    const TileOut o{op, ostep, c, active && p.out != nullptr, has_z, Dv};
+    const TileOut o{op, ostep, c, active && p.out != nullptr, has_z, Dv, (p.flags & LBS_FLAG_ACCUM) != 0};
     for (int t0 = 0; t0 < clen; t0 += m) {
       const int r = min(m, clen - t0);
       if (p.ckpt != nullptr && active && (c + t0) % p.ckpt_len == 0) {

@@ -139,7 +139,7 @@ def _flags(delta_softplus, reverse, lb, mode):
 def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
                            delta_softplus=True, window=None, reverse=False,
                            return_last_state=False, lb=True, discretize_mode="exp",
-                           out=None, seg_hint=0, save_checkpoints=False):
+                           out=None, seg_hint=0, save_checkpoints=False, accumulate=False):
     """Forward launch (no autograd).  Returns ``out`` or ``(out, last_state)``;
     with ``save_checkpoints`` a trailing fp32 checkpoint buffer for
     :func:`lbm_selective_scan_bwd` is appended."""
@@ -149,6 +149,8 @@ def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
         out = torch.empty((Bt, L, E), dtype=u.dtype, device=u.device)
     last = torch.empty((Bt, E, N), dtype=torch.float32, device=u.device) if return_last_state else None
     flags = _flags(delta_softplus, reverse, lb, discretize_mode)
+    if accumulate:
+        flags |= _lib.FLAG_ACCUM
     args = _fwd_args(u, delta, A, B, C, D, z, delta_bias, M, dims, flags, out, last, seg_hint)
     L_ = _lib.lib()
     ck = None
@@ -245,3 +247,22 @@ def selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None, delta_sof
     # forward-only kernel on its fast full-tile path
     return lbm_selective_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8, reverse,
                               return_last_state, "exp", lb=False)
+
+
+def global_bidir_selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=None, *,
+                                delta_b=None, A_b=None, B_b=None, C_b=None, D_b=None,
+                                delta_bias_b=None, delta_softplus=True, return_last_state=False):
+    """Vim-style globally bi-directional selective scan — the baseline LBMamba is
+    measured against (engine.global_bidir_par, engine.py:305-327; oracle.py:71-77):
+    a full forward sweep with (delta, A, B, C, D, delta_bias) plus a full
+    right-to-left sweep (flip-on-load) with the ``*_b`` parameters, summed, gated
+    by silu(z).  Two launches of the forward-only kernel, the second accumulating
+    into the first's output; ``last_state`` is h_f + h_b like the reference."""
+    out, hf = lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8, False,
+                                     True, False)
+    pb = dict(delta=delta if delta_b is None else delta_b, A=A if A_b is None else A_b,
+              B=B if B_b is None else B_b, C=C if C_b is None else C_b, D=D if D_b is None else D_b,
+              delta_bias=delta_bias if delta_bias_b is None else delta_bias_b)
+    _, hb = lbm_selective_scan_fwd(u, pb["delta"], pb["A"], pb["B"], pb["C"], pb["D"], z, pb["delta_bias"],
+                                   delta_softplus, 8, True, True, False, out=out, accumulate=True)
+    return (out, hf + hb) if return_last_state else out

@@ -291,3 +291,26 @@ def test_fused_vectorised_path_state_sizes(N):
         ref, rhf = O.lbm_selective_scan(**inp, window=8, reverse=reverse, return_last_state=True)
         assert O.max_rel_err(got, ref) <= TOL_F32
         assert O.max_rel_err(hf, rhf) <= TOL_F32
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_global_bidir_fused(dtype):
+    """Vim-style global bi-directional baseline (engine.global_bidir_par,
+    engine.py:305-327) on the fused op: forward sweep + flip-on-load backward
+    sweep with separate parameters, summed, gated."""
+    from paper_2506_15976_b200.scan import global_bidir_selective_scan
+    inp = op_inputs(50, 2, 150, 64, 16)
+    pb = op_inputs(51, 2, 150, 64, 16)
+    if dtype != torch.float32:
+        inp = quantize(inp, dtype)
+        pb = quantize(pb, dtype)
+    t = {k: (dev(v, dtype) if k in ("u", "delta", "z", "B", "C") else dev(v)) for k, v in inp.items()}
+    tb = {k: (dev(v, dtype) if k in ("delta", "B", "C") else dev(v)) for k, v in pb.items()}
+    out, h = global_bidir_selective_scan(**t, delta_b=tb["delta"], A_b=tb["A"], B_b=tb["B"], C_b=tb["C"],
+                                         D_b=tb["D"], delta_bias_b=tb["delta_bias"], return_last_state=True)
+    fb = dict(inp, delta=pb["delta"], A=pb["A"], B=pb["B"], C=pb["C"], D=pb["D"], delta_bias=pb["delta_bias"])
+    rf, hf = O.lbm_selective_scan(**inp, lb=False, return_last_state=True)
+    rb, hb = O.lbm_selective_scan(**fb, lb=False, reverse=True, return_last_state=True)
+    tol = TOL_F32 if dtype == torch.float32 else TOL_BF16
+    assert O.max_rel_err(out.float().cpu().numpy(), rf + rb) <= tol
+    assert O.max_rel_err(h.cpu().numpy(), hf + hb) <= tol
