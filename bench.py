@@ -232,7 +232,17 @@ def measure_ops(peak, iters=10):
             del dout, ck
         res[name] = r
         del x, out
-    del flush
+    # configs[3] at model level: LBVim-S 1024^2 (L = 4096 + class token), batch 32, bf16 forward
+    from paper_2506_15976_b200 import model as M
+    cfg = M.lbvim_small(image_size=1024)
+    net = M.LBVim(cfg, M.init_params(cfg, seed=0), dtype=torch.bfloat16)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    imgs = torch.randn(32, 1024, 1024, 3, generator=g, device="cuda").to(torch.bfloat16)
+    run = net.graphed(imgs)
+    ms = time_fn(run, 3, flush)
+    res["cfg4_model"] = {"what": "configs[3] LBVim-S 1024^2 patch16 forward, batch 32, bf16, 24 layers, L=4097",
+                         "ms_per_batch": ms, "images_per_s": 32 / ms * 1e3}
+    del net, imgs, run, flush
     torch.cuda.empty_cache()
     return res
 

@@ -94,6 +94,8 @@ int validate_fwd(const lbs_scan_fwd_args* a) {
       return fail(LBS_ERR_UNSUPPORTED, "effective window min(window, L) = %lld > 16 is not supported",
                   (long long)m);
   }
+  if ((a->flags & LBS_FLAG_ACCUM) && (a->flags & LBS_FLAG_LB))
+    return fail(LBS_ERR_UNSUPPORTED, "LBS_FLAG_ACCUM is supported for the forward-only scan (no LBS_FLAG_LB)");
   if (a->checkpoints && a->ckpt_len != lbs_scan_ckpt_len(a->seqlen, a->window))
     return fail(LBS_ERR_INVALID, "ckpt_len %lld != lbs_scan_ckpt_len(L, window) = %lld", (long long)a->ckpt_len,
                 (long long)lbs_scan_ckpt_len(a->seqlen, a->window));

@@ -37,6 +37,10 @@
 
 namespace lbs {
 
+#ifndef LBS_BWD_RED_SMEM
+#define LBS_BWD_RED_SMEM 1  // dB/dC warp sums by shared-memory transpose (else shuffle reduce-scatter)
+#endif
+
 constexpr int kBwdThreads = kFwdThreads;  // BcPrefetch assumes 128 threads
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -61,7 +65,9 @@ struct BwdSmem {
   static constexpr size_t off_da = off_mu + pq_bytes;
   static constexpr size_t off_red = off_da + pq_bytes;
   static constexpr size_t off_raw = off_red + red_bytes;
-  static constexpr size_t total = off_raw + raw_bytes;
+  static constexpr size_t tr_bytes = 4ull * (KT * 4) * 33 * sizeof(float);  // per-warp transpose [v][lane]
+  static constexpr size_t off_tr = off_raw + raw_bytes;
+  static constexpr size_t total = off_tr + tr_bytes;
 };
 
 // u / delta / z / dout rows of one chunk -> ring stage (see SeqStager).
@@ -157,7 +163,7 @@ template <typename Tio, int NS, int KT, bool kLB, bool kFull, bool kOneTile>
 __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx& x, const Tio* su,
                                           const Tio* sd, const Tio* sz, const Tio* sg,
                                           const float* bcf, const f2* ck, const f2* a2s, f2* mu,
-                                          f2* dAs, float* red, float& dD_acc, float& dbias_acc,
+                                          f2* dAs, float* red, float* tr, float& dD_acc, float& dbias_acc,
                                           Tio* dup, Tio* ddp, Tio* dzp, long long sdu, long long sdd,
                                           long long sdz) {
   constexpr int NP = NS / 2;
@@ -251,6 +257,15 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
         lam = lamj;
         Qn = Qc;
       }
+#if LBS_BWD_RED_SMEM
+      // park the 4 values of step j in this warp's transpose buffer [v][lane]
+      float* tw = tr + (size_t)warp * (KT * 4) * 33;
+      tw[(j * 4 + 0) * 33 + lane] = dBv.x;
+      tw[(j * 4 + 1) * 33 + lane] = dBv.y;
+      tw[(j * 4 + 2) * 33 + lane] = dCv.x;
+      tw[(j * 4 + 3) * 33 + lane] = dCv.y;
+      (void)rv;
+#else
       const int o = (j & 3) * 4;
       rv[o + 0] = dBv.x;
       rv[o + 1] = dBv.y;
@@ -264,7 +279,30 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
           red[((warp * KT + jj) * 2 + (kind >> 1)) * NS + 2 * q + (kind & 1)] = s;
         }
       }
+#endif
     }
+#if LBS_BWD_RED_SMEM
+    // warp sum of each of the KT*4 values: lane l owns values l, l+32, ...
+    __syncwarp();
+    {
+      const float* tw = tr + (size_t)warp * (KT * 4) * 33;
+#pragma unroll
+      for (int v0 = 0; v0 < KT * 4; v0 += 32) {
+        const int vv = v0 + lane;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          s0 += tw[vv * 33 + k];
+          s1 += tw[vv * 33 + k + 1];
+          s2 += tw[vv * 33 + k + 2];
+          s3 += tw[vv * 33 + k + 3];
+        }
+        const int jj = vv >> 2, kind = vv & 3;
+        red[((warp * KT + jj) * 2 + (kind >> 1)) * NS + 2 * q + (kind & 1)] = (s0 + s1) + (s2 + s3);
+      }
+    }
+    __syncwarp();
+#endif
     // carry into the previous chunk: a_{c} * lam_{c}
     mu[q * kBwdThreads + tid] = mul2(a[0], lam);
     dAs[q * kBwdThreads + tid] = add2(dAs[q * kBwdThreads + tid], dAq);
@@ -316,6 +354,7 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
   f2* dAs = reinterpret_cast<f2*>(smem_raw + Sm::off_da);
   float* red = reinterpret_cast<float*>(smem_raw + Sm::off_red);
   Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::off_raw);
+  float* trs = reinterpret_cast<float*>(smem_raw + Sm::off_tr);
 
   const FwdParams& p = P.f;
   const int tid = threadIdx.x;
@@ -417,7 +456,7 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
     const Tio* sg = base + 3 * KT * kBwdThreads;
     const f2* ck = cks + stg * NP * kBwdThreads;
 #define LBS_BWD_CHUNK(FULL, ONE)                                                                     \
-  bwd_chunk<Tio, NS, KT, kLB, FULL, ONE>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, dD_acc, dbias_acc, \
+  bwd_chunk<Tio, NS, KT, kLB, FULL, ONE>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, trs, dD_acc, dbias_acc, \
                                          dup, ddp, dzp, sdu, sdd, sdz)
     if (one_tile) {
       if (clen == KT) LBS_BWD_CHUNK(true, true);

@@ -413,7 +413,7 @@ struct StateStore {
   }
 };
 
-template <typename Tio, int NS, int MT, bool kLB, bool kFull, int QU, bool kRegs>
+template <typename Tio, int NS, int MT, bool kLB, bool kFull, int QU, bool kRegs, bool kAccum = false>
 __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const Tio* sz,
                                              const float* bcf, const f2* a2s, StateStore<NS / 2, kRegs>& h,
                                              int t0, int r, float bias, bool softplus, bool linear,
@@ -422,6 +422,14 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
   const int tid = threadIdx.x;
   float dl[MT], du[MT];
   f2 yacc[MT];
+  // LBS_FLAG_ACCUM: the previous outputs of this tile are loaded before the
+  // pair loop so the read latency hides under the tile's compute
+  float prev[kAccum ? MT : 1];
+  if (kAccum && o.active) {
+    const Tio* opp = static_cast<const Tio*>(o.op);
+#pragma unroll
+    for (int j = 0; j < MT; ++j) prev[j] = (kFull || j < r) ? to_f(opp[(long long)(o.c + t0 + j) * o.step]) : 0.f;
+  }
 #pragma unroll
   for (int j = 0; j < MT; ++j) {
     const bool on = kFull || j < r;
@@ -480,7 +488,7 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 #else
         if (o.has_z) y *= silu_f(to_f(sz[(t0 + j) * kFwdThreads + tid]));
         Tio* dst = op + (long long)(o.c + t0 + j) * o.step;
-        if (o.accum) y += to_f(*dst);
+        if constexpr (kAccum) y += prev[j];
         st<Tio>(dst, y);
 #endif
       }
@@ -501,7 +509,7 @@ constexpr int fwd_chunk(int mt) { return mt > LBS_FWD_CL ? mt : LBS_FWD_CL; }
 #define LBS_FWD_MINB16 2
 #endif
 
-template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec>
+template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec, bool kAccum = false>
 __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16)) fwd_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
   constexpr int CL = fwd_chunk(MT);
@@ -600,7 +608,7 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
         for (int q = 0; q < NP; ++q) ck[(long long)q * p.E] = h.get(q);
       }
       if (r == MT)
-        tile_compute<Tio, NS, MT, kLB, true, QU, kRegs>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, true, QU, kRegs, kAccum>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
       else {
         // ragged tile (at most once per segment): rolled pair loop on the smem state
         StateStore<NP, false> hp;
@@ -609,7 +617,7 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
 #pragma unroll
           for (int q = 0; q < NP; ++q) hp.set(q, h.get(q));
         }
-        tile_compute<Tio, NS, MT, kLB, false, 1, false>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, false, 1, false, kAccum>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
         if constexpr (kRegs) {
 #pragma unroll
           for (int q = 0; q < NP; ++q) h.set(q, hp.get(q));
@@ -742,8 +750,11 @@ inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
     k1<<<g1, block, smem1, st>>>(p);
   }
   dim3 grid((p.E + kFwdThreads - 1) / kFwdThreads, p.Bt, p.n_seg);
-  auto k = (p.flags & LBS_FLAG_LB) ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec>
-                                   : fwd_kernel<Tio, Tbc, NS, MT, false, kVec>;
+  // LBS_FLAG_ACCUM is instantiated for the forward-only scan (the global-bidir
+  // baseline's second sweep); the C ABI rejects ACCUM together with LB
+  auto k = (p.flags & LBS_FLAG_LB)      ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec>
+           : (p.flags & LBS_FLAG_ACCUM) ? fwd_kernel<Tio, Tbc, NS, MT, false, kVec, true>
+                                        : fwd_kernel<Tio, Tbc, NS, MT, false, kVec>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, block, smem, st>>>(p);
   return cudaGetLastError();
