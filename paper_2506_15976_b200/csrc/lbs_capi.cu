@@ -39,23 +39,26 @@ constexpr int kNumSMs = 148;
 // states padded per thread (kernels instantiate NS in {4, 16})
 int padded_states(int64_t N) { return N <= 4 ? 4 : 16; }
 
-// Sequence-split plan: cut L into S segments (multiples of the window) only
-// when B*E alone cannot fill the machine; each extra segment costs one extra
-// aggregate pass over its steps, so S stays as small as possible.
-void plan_segments(const lbs_scan_fwd_args* a, int* n_seg, int* seg_len) {
-  const int64_t L = a->seqlen, m = a->window;
-  const int64_t ctas = ((a->dim + lbs::kFwdThreads - 1) / lbs::kFwdThreads) * a->batch;
+// Launch plan of the forward.
+//  * CTA width: 128 channels, or 64 when channels are scarce (E <= 64, or fewer
+//    than two 128-wide CTAs per SM) — no idle threads, finer balance over SMs.
+//  * Sequence split: cut L into S segments (multiples of the window) only when
+//    B*E alone cannot fill the machine (~8 resident warps per SM); each extra
+//    segment costs one aggregate pass over its steps, so S stays minimal.  The
+//    segments are stitched by a parallel prefix over their aggregates.
+void plan_fwd(const lbs_scan_fwd_args* a, int* cta, int* n_seg, int* seg_len) {
+  const int64_t L = a->seqlen, m = a->window < a->seqlen ? a->window : a->seqlen;
+  const int64_t ctas128 = ((a->dim + 127) / 128) * a->batch;
+  *cta = (a->dim <= 64 || ctas128 < 2 * kNumSMs) ? 64 : 128;
   const int64_t warps = ((a->dim + 31) / 32) * a->batch;
   int64_t S = 1;
   if (a->seg_hint > 0) {
     S = a->seg_hint;
   } else if (warps < 4 * kNumSMs && L >= 1024) {
-    // aim for ~8 resident warps per SM, segments no shorter than 256 steps
     S = (8 * kNumSMs + warps - 1) / warps;
-    (void)ctas;
-    const int64_t max_s = L / 256;
+    const int64_t max_s = L / 128;  // segments no shorter than 128 steps
     if (S > max_s) S = max_s;
-    if (S > 256) S = 256;
+    if (S > 2048) S = 2048;
     if (S < 1) S = 1;
   }
   int64_t len = (L + S - 1) / S;
@@ -63,6 +66,11 @@ void plan_segments(const lbs_scan_fwd_args* a, int* n_seg, int* seg_len) {
   S = (L + len - 1) / len;
   *n_seg = (int)S;
   *seg_len = (int)len;
+}
+
+void plan_segments(const lbs_scan_fwd_args* a, int* n_seg, int* seg_len) {
+  int cta;
+  plan_fwd(a, &cta, n_seg, seg_len);
 }
 
 int validate_fwd(const lbs_scan_fwd_args* a) {
@@ -237,7 +245,7 @@ int lbs_scan_fwd(const lbs_scan_fwd_args* a, void* ws, size_t ws_bytes, void* st
   fill_fwd_params(a, &p);
   lbs_scan_fwd_args b = *a;
   b.window = p.m;
-  plan_segments(&b, &p.n_seg, &p.seg_len);
+  plan_fwd(&b, &p.cta, &p.n_seg, &p.seg_len);
   if (p.n_seg > 1) {
     const size_t need = (size_t)a->batch * p.n_seg * a->dim * 2 * padded_states(a->dstate) * sizeof(float);
     if (!ws || ws_bytes < need)
@@ -320,7 +328,7 @@ int lbs_scan_bwd(const lbs_scan_bwd_args* a, void* ws, size_t ws_bytes, void* st
     fp.z = lbs::View3D{nullptr, 0, 0, 0};
     lbs_scan_fwd_args b2 = *f;
     b2.window = fp.m;
-    plan_segments(&b2, &fp.n_seg, &fp.seg_len);
+    plan_fwd(&b2, &fp.cta, &fp.n_seg, &fp.seg_len);
     if (fp.n_seg > 1) fp.seg_agg = reinterpret_cast<float*>(w + lay.off_seg);
     rc = cuda_status(lbs::launch_fwd(fp, f->io_dtype, f->bc_dtype, st), "lbs_scan_bwd (recompute)");
     if (rc != LBS_OK) return rc;

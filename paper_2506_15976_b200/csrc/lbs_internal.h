@@ -24,7 +24,8 @@ struct FwdParams {
   const float* D;
   const float* bias;
   float* last_state;
-  // sequence split
+  // CTA width (128, or 64 for low channel parallelism) and sequence split
+  int cta;
   int n_seg, seg_len;
   float* seg_agg;  // (Bt, n_seg, E, 2*NS) fp32 workspace
   // training checkpoints (state entering each ckpt chunk)

@@ -49,12 +49,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define LBS_FWD_CL 16  // steps per staged chunk (raised to the tile length for long windows)
 #endif
 
-template <typename Tio, int CLv = LBS_FWD_CL>
+template <typename Tio, int CLv = LBS_FWD_CL, int CT = kFwdThreads>
 struct FwdCfg {
   static constexpr int CL = CLv;                               // max steps per chunk
-  static constexpr int PPR = kFwdThreads * sizeof(Tio) / 16;  // 16-byte pieces per ring row
+  static constexpr int PPR = CT * sizeof(Tio) / 16;  // 16-byte pieces per ring row
   static constexpr int EPP = 16 / sizeof(Tio);                // elements per piece
-  static constexpr int RS = kFwdThreads / PPR;                 // ring rows covered per pass
+  static constexpr int RS = CT / PPR;                 // ring rows covered per pass
   static constexpr int KP = (CL + RS - 1) / RS;                // pieces per thread per array
 };
 
@@ -63,14 +63,14 @@ struct FwdCfg {
 //   bcf[CL][2*NS]                      (f32)   B then C per step, zero padded
 //   a2s[NS/2][128]                     (f2)    A*log2(e) per channel pair
 //   bcraw[2 stages][CL][2*NS]           (Tbc)   B|C rows as loaded (cp.async path)
-template <typename Tio, typename Tbc, int NS, int CLv = LBS_FWD_CL>
+template <typename Tio, typename Tbc, int NS, int CLv = LBS_FWD_CL, int CT = kFwdThreads>
 struct FwdSmem {
   static constexpr int CL = CLv;
-  static constexpr size_t seq_bytes = 2ull * 3 * CL * kFwdThreads * sizeof(Tio);
+  static constexpr size_t seq_bytes = 2ull * 3 * CL * CT * sizeof(Tio);
   static constexpr size_t bc_bytes = (size_t)CL * 2 * NS * sizeof(float);
-  static constexpr size_t a2_bytes = (size_t)(NS / 2) * kFwdThreads * sizeof(f2);
+  static constexpr size_t a2_bytes = (size_t)(NS / 2) * CT * sizeof(f2);
   static constexpr size_t raw_bytes = 2ull * CL * 2 * NS * sizeof(Tbc);
-  static constexpr size_t hs_bytes = (size_t)(NS / 2) * kFwdThreads * sizeof(f2);  // state spill area
+  static constexpr size_t hs_bytes = (size_t)(NS / 2) * CT * sizeof(f2);  // state spill area
   static constexpr size_t total = seq_bytes + bc_bytes + a2_bytes + raw_bytes + hs_bytes;
 };
 
@@ -78,9 +78,9 @@ struct FwdSmem {
 // thread owns one fixed piece column and rows t = row0 + k*RS, so all index
 // math is hoisted out of the chunk loop; "logical step l" addresses
 // base + l*step (step < 0 for the reverse direction = flip-on-load).
-template <typename Tio, bool kVec, int CLv = LBS_FWD_CL>
+template <typename Tio, bool kVec, int CLv = LBS_FWD_CL, int CT = kFwdThreads>
 struct SeqStager {
-  using C = FwdCfg<Tio, CLv>;
+  using C = FwdCfg<Tio, CLv, CT>;
   const Tio* base[3];
   long long step[3];
   int narr, row0, col;
@@ -112,15 +112,15 @@ struct SeqStager {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (a >= narr) break;
-      Tio* dst = seq + ((size_t)(stg * 3 + a) * C::CL) * kFwdThreads + col;
+      Tio* dst = seq + ((size_t)(stg * 3 + a) * C::CL) * CT + col;
       if constexpr (kVec) {
 #pragma unroll
         for (int k = 0; k < C::KP; ++k) {
           const int t = row0 + k * C::RS;
-          if (t < clen) cp_async16(dst + t * kFwdThreads, base[a] + (long long)(c + t) * step[a]);
+          if (t < clen) cp_async16(dst + t * CT, base[a] + (long long)(c + t) * step[a]);
         }
       } else {
-        for (int t = 0; t < clen; ++t) dst[t * kFwdThreads] = base[a][(long long)(c + t) * step[a]];
+        for (int t = 0; t < clen; ++t) dst[t * CT] = base[a][(long long)(c + t) * step[a]];
       }
     }
   }
@@ -138,10 +138,10 @@ __host__ __device__ constexpr int bc_index(int t, int w, int n) {
   return kIL ? t * 2 * NS + (n >> 1) * 4 + w * 2 + (n & 1) : t * 2 * NS + w * NS + n;
 }
 
-template <typename Tbc, int NS, int CL, bool kIL = false>
+template <typename Tbc, int NS, int CL, bool kIL = false, int CT = kFwdThreads>
 struct BcPrefetch {
   static constexpr int W = 2 * NS;                  // values per step
-  static constexpr int RS = kFwdThreads / W;        // rows per pass
+  static constexpr int RS = CT / W;        // rows per pass
   static constexpr int BCR = (CL + RS - 1) / RS;    // values per thread
   float v[BCR];
   const Tbc* base;
@@ -184,11 +184,11 @@ struct BcPrefetch {
 // raw rows are copied by cp.async into a 2-stage shared-memory ring together
 // with u/delta/z — a global load the compiler cannot sink to its use — and
 // converted to the fp32 broadcast table at publish.  Otherwise: BcPrefetch.
-template <typename Tbc, int NS, int CL, bool kAsync, bool kIL = false>
+template <typename Tbc, int NS, int CL, bool kAsync, bool kIL = false, int CT = kFwdThreads>
 struct BcStage {
   static constexpr int EPB = 16 / sizeof(Tbc);   // elements per 16-byte piece
   static constexpr int PB = NS / EPB;            // pieces per B (or C) row
-  BcPrefetch<Tbc, NS, CL, kIL> pre;
+  BcPrefetch<Tbc, NS, CL, kIL, CT> pre;
   const Tbc* base[2];
   long long step;
   __device__ __forceinline__ void init(const FwdParams& p, int b) {
@@ -203,9 +203,9 @@ struct BcStage {
   }
   __device__ __forceinline__ void issue(Tbc* raw, int stg, int c, int clen) {
     if constexpr (kAsync) {
-      static_assert(CL * 2 * PB <= kFwdThreads || (CL * 2 * PB) % kFwdThreads == 0, "piece split");
+      static_assert(CL * 2 * PB <= CT || (CL * 2 * PB) % CT == 0, "piece split");
 #pragma unroll
-      for (int i0 = 0; i0 < CL * 2 * PB; i0 += kFwdThreads) {
+      for (int i0 = 0; i0 < CL * 2 * PB; i0 += CT) {
         const int i = i0 + threadIdx.x;
         const int t = i / (2 * PB), r = i % (2 * PB);
         const int w = r / PB, piece = r % PB;
@@ -220,7 +220,7 @@ struct BcStage {
   __device__ __forceinline__ void publish(float* bcf, const Tbc* raw, int stg, int clen) {
     if constexpr (kAsync) {
 #pragma unroll
-      for (int i0 = 0; i0 < CL * 2 * NS; i0 += kFwdThreads) {
+      for (int i0 = 0; i0 < CL * 2 * NS; i0 += CT) {
         const int i = i0 + threadIdx.x;
         const int t = i / (2 * NS), kk = i % (2 * NS);
         if (i < CL * 2 * NS)  // (CL * 2 * NS may be < the 128 threads, e.g. N = 4 in the backward)
@@ -402,20 +402,21 @@ __device__ __forceinline__ void pair_chains(f2& hq, const f2 (&a)[MT], int q, co
 // Fixed-size state store of a thread: registers (QU == NP: every loop over q is
 // unrolled) or this thread's column of a shared-memory array [NP][128] (QU < NP:
 // the pair loop stays rolled, which keeps the kernel's code in the I-cache).
-template <int NP, bool kRegs>
+template <int NP, bool kRegs, int CT = kFwdThreads>
 struct StateStore {
   f2 r[kRegs ? NP : 1];
   f2* s;
-  __device__ __forceinline__ f2 get(int q) const { return kRegs ? r[kRegs ? q : 0] : s[q * kFwdThreads + threadIdx.x]; }
+  __device__ __forceinline__ f2 get(int q) const { return kRegs ? r[kRegs ? q : 0] : s[q * CT + threadIdx.x]; }
   __device__ __forceinline__ void set(int q, f2 v) {
     if constexpr (kRegs) r[q] = v;
-    else s[q * kFwdThreads + threadIdx.x] = v;
+    else s[q * CT + threadIdx.x] = v;
   }
 };
 
-template <typename Tio, int NS, int MT, bool kLB, bool kFull, int QU, bool kRegs, bool kAccum = false>
+template <typename Tio, int NS, int MT, bool kLB, bool kFull, int QU, bool kRegs, bool kAccum = false,
+          int CT = kFwdThreads>
 __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const Tio* sz,
-                                             const float* bcf, const f2* a2s, StateStore<NS / 2, kRegs>& h,
+                                             const float* bcf, const f2* a2s, StateStore<NS / 2, kRegs, CT>& h,
                                              int t0, int r, float bias, bool softplus, bool linear,
                                              const TileOut& o) {
   constexpr int NP = NS / 2;
@@ -433,8 +434,8 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 #pragma unroll
   for (int j = 0; j < MT; ++j) {
     const bool on = kFull || j < r;
-    float d = on ? to_f(sd[(t0 + j) * kFwdThreads + tid]) + bias : 0.f;
-    const float uv = on ? to_f(su[(t0 + j) * kFwdThreads + tid]) : 0.f;
+    float d = on ? to_f(sd[(t0 + j) * CT + tid]) + bias : 0.f;
+    const float uv = on ? to_f(su[(t0 + j) * CT + tid]) : 0.f;
 #if !LBS_DBG_NOSOFTPLUS
     if (softplus) d = softplus_f(d);
 #endif
@@ -445,20 +446,20 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
   if constexpr (kRegs) {
 #pragma unroll
     for (int q = 0; q < NP; ++q)
-      pair_tile<NS, MT, kLB, kFull>(h.r[q], a2s[q * kFwdThreads + tid], q, dl, du, yacc, bcf, t0, r, linear);
+      pair_tile<NS, MT, kLB, kFull>(h.r[q], a2s[q * CT + tid], q, dl, du, yacc, bcf, t0, r, linear);
   } else if constexpr (LBS_PIPE && kFull && MT <= 8 && LBS_BC_IL && NP % 2 == 0) {
     // two-stage pipeline over state pairs, unrolled by 2 so the buffers swap names
     f2 aA[MT], aB[MT];
     pair_exps<NS, MT>(aA, a2s[tid], dl, linear);
 #pragma unroll 1
     for (int q = 0; q < NP; q += 2) {
-      pair_exps<NS, MT>(aB, a2s[(q + 1) * kFwdThreads + tid], dl, linear);
+      pair_exps<NS, MT>(aB, a2s[(q + 1) * CT + tid], dl, linear);
       {
         f2 hq = h.get(q);
         pair_chains<NS, MT, kLB>(hq, aA, q, du, yacc, bcf, t0);
         h.set(q, hq);
       }
-      if (q + 2 < NP) pair_exps<NS, MT>(aA, a2s[(q + 2) * kFwdThreads + tid], dl, linear);
+      if (q + 2 < NP) pair_exps<NS, MT>(aA, a2s[(q + 2) * CT + tid], dl, linear);
       {
         f2 hq = h.get(q + 1);
         pair_chains<NS, MT, kLB>(hq, aB, q + 1, du, yacc, bcf, t0);
@@ -472,7 +473,7 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
       for (int qq = 0; qq < QU; ++qq) {
         const int q = q0 + qq;
         f2 hq = h.get(q);
-        pair_tile<NS, MT, kLB, kFull>(hq, a2s[q * kFwdThreads + tid], q, dl, du, yacc, bcf, t0, r, linear);
+        pair_tile<NS, MT, kLB, kFull>(hq, a2s[q * CT + tid], q, dl, du, yacc, bcf, t0, r, linear);
         h.set(q, hq);
       }
     }
@@ -486,7 +487,7 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 #if LBS_DBG_NOSTORE  // ablation only
         if (y == 1234.5f) st<Tio>(op + (long long)(o.c + t0 + j) * o.step, y);
 #else
-        if (o.has_z) y *= silu_f(to_f(sz[(t0 + j) * kFwdThreads + tid]));
+        if (o.has_z) y *= silu_f(to_f(sz[(t0 + j) * CT + tid]));
         Tio* dst = op + (long long)(o.c + t0 + j) * o.step;
         if constexpr (kAccum) y += prev[j];
         st<Tio>(dst, y);
@@ -509,11 +510,12 @@ constexpr int fwd_chunk(int mt) { return mt > LBS_FWD_CL ? mt : LBS_FWD_CL; }
 #define LBS_FWD_MINB16 2
 #endif
 
-template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec, bool kAccum = false>
-__global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16)) fwd_kernel(FwdParams p) {
+template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec, bool kAccum = false, int CT = kFwdThreads>
+__global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) * (kFwdThreads / CT))
+    fwd_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
   constexpr int CL = fwd_chunk(MT);
-  using Sm = FwdSmem<Tio, Tbc, NS, CL>;
+  using Sm = FwdSmem<Tio, Tbc, NS, CL, CT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
   constexpr bool kRegs = QU >= NP;
 
   const int tid = threadIdx.x;
-  const int e0 = blockIdx.x * kFwdThreads;
+  const int e0 = blockIdx.x * CT;
   const int e = e0 + tid;
   const int b = blockIdx.y;
   const int seg = blockIdx.z;
@@ -544,22 +546,20 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
     float a0 = 2 * q < N ? p.A[(long long)ec * N + 2 * q] : 0.f;
     float a1 = 2 * q + 1 < N ? p.A[(long long)ec * N + 2 * q + 1] : 0.f;
     if (!linear) { a0 *= kLog2e; a1 *= kLog2e; }
-    a2s[q * kFwdThreads + tid] = mk2(a0, a1);
+    a2s[q * CT + tid] = mk2(a0, a1);
   }
   const float Dv = p.D ? p.D[ec] : 0.f;
   const float bias = p.bias ? p.bias[ec] : 0.f;
 
-  StateStore<NP, kRegs> h;
+  StateStore<NP, kRegs, CT> h;
   h.s = hsm;
 #pragma unroll
   for (int q = 0; q < NP; ++q) h.set(q, mk2(0.f, 0.f));
   if (seg > 0) {
-    const float* agg = p.seg_agg;
-    for (int s = 0; s < seg; ++s) {
-      const f2* PH = reinterpret_cast<const f2*>(agg + ((((long long)b * p.n_seg + s) * p.E + ec) * (2 * NS)));
+    // state entering this segment: folded over the earlier segments by segment_prefix_kernel
+    const f2* PH = reinterpret_cast<const f2*>(p.seg_agg + ((((long long)b * p.n_seg + seg - 1) * p.E + ec) * (2 * NS)));
 #pragma unroll
-      for (int q = 0; q < NP; ++q) h.set(q, fma2(PH[q], h.get(q), PH[NP + q]));
-    }
+    for (int q = 0; q < NP; ++q) h.set(q, PH[NP + q]);
   }
 
   // p.out == nullptr: checkpoint-only sweep (the backward's recompute pass)
@@ -568,9 +568,9 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
                                    (rev ? (long long)(L - 1) * p.so1 : 0);
   const long long ostep = rev ? -p.so1 : p.so1;
 
-  SeqStager<Tio, kVec, CL> stager;
+  SeqStager<Tio, kVec, CL, CT> stager;
   stager.init(p, b, e0, has_z);
-  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL> bcs;
+  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL, CT> bcs;
   bcs.init(p, b);
   // prologue: chunk 0
   int c = seg_lo;
@@ -593,9 +593,9 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
     cp_async_commit();
     __syncthreads();  // bcf visible
 
-    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * kFwdThreads;
-    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * kFwdThreads;
-    const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * kFwdThreads;
+    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * CT;
+    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * CT;
+    const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * CT;
     const TileOut o{op, ostep, c, active && p.out != nullptr, has_z, Dv, (p.flags & LBS_FLAG_ACCUM) != 0};
     for (int t0 = 0; t0 < clen; t0 += m) {
       const int r = min(m, clen - t0);
@@ -608,16 +608,16 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
         for (int q = 0; q < NP; ++q) ck[(long long)q * p.E] = h.get(q);
       }
       if (r == MT)
-        tile_compute<Tio, NS, MT, kLB, true, QU, kRegs, kAccum>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, true, QU, kRegs, kAccum, CT>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
       else {
         // ragged tile (at most once per segment): rolled pair loop on the smem state
-        StateStore<NP, false> hp;
+        StateStore<NP, false, CT> hp;
         hp.s = hsm;
         if constexpr (kRegs) {
 #pragma unroll
           for (int q = 0; q < NP; ++q) hp.set(q, h.get(q));
         }
-        tile_compute<Tio, NS, MT, kLB, false, 1, false, kAccum>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, false, 1, false, kAccum, CT>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
         if constexpr (kRegs) {
 #pragma unroll
           for (int q = 0; q < NP; ++q) h.set(q, hp.get(q));
@@ -642,11 +642,11 @@ __global__ void __launch_bounds__(kFwdThreads, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD
 // Pass 1 of the sequence split: per (b, segment, e, n) the segment's
 // aggregate affine map h -> P*h + H with P = prod a = exp(A * sum delta) and
 // H the local end state from zero (core.py:48-55 combine, applied serially).
-template <typename Tio, typename Tbc, int NS, bool kVec>
-__global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p) {
+template <typename Tio, typename Tbc, int NS, bool kVec, int CT = kFwdThreads>
+__global__ void __launch_bounds__(CT) segment_state_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
   constexpr int CL = LBS_FWD_CL;
-  using Sm = FwdSmem<Tio, Tbc, NS, CL>;
+  using Sm = FwdSmem<Tio, Tbc, NS, CL, CT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
   Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes);
 
   const int tid = threadIdx.x;
-  const int e0 = blockIdx.x * kFwdThreads;
+  const int e0 = blockIdx.x * CT;
   const int e = e0 + tid;
   const int b = blockIdx.y;
   const int seg = blockIdx.z;
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
     float a0 = 2 * q < N ? p.A[(long long)ec * N + 2 * q] : 0.f;
     float a1 = 2 * q + 1 < N ? p.A[(long long)ec * N + 2 * q + 1] : 0.f;
     if (!linear) { a0 *= kLog2e; a1 *= kLog2e; }
-    a2s[q * kFwdThreads + tid] = mk2(a0, a1);
+    a2s[q * CT + tid] = mk2(a0, a1);
   }
   const float bias = p.bias ? p.bias[ec] : 0.f;
   f2 H[NP], P[NP];
@@ -680,9 +680,9 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
   for (int q = 0; q < NP; ++q) { H[q] = mk2(0.f, 0.f); P[q] = mk2(1.f, 1.f); }
   float dsum = 0.f;
 
-  SeqStager<Tio, kVec> stager;
+  SeqStager<Tio, kVec, LBS_FWD_CL, CT> stager;
   stager.init(p, b, e0, false);
-  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL> bcs;
+  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL, CT> bcs;
   bcs.init(p, b);
   int c = seg_lo;
   int clen = min(CL, seg_hi - c);
@@ -702,16 +702,16 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
     }
     cp_async_commit();
     __syncthreads();
-    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * kFwdThreads;
-    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * kFwdThreads;
+    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * CT;
+    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * CT;
     for (int t = 0; t < clen; ++t) {
-      float dl = to_f(sd[t * kFwdThreads + tid]) + bias;
+      float dl = to_f(sd[t * CT + tid]) + bias;
       if (softplus) dl = softplus_f(dl);
-      const float du = dl * to_f(su[t * kFwdThreads + tid]);
+      const float du = dl * to_f(su[t * CT + tid]);
       dsum += dl;
 #pragma unroll
       for (int q = 0; q < NP; ++q) {
-        const f2 x = mul2(bc2(dl), a2s[q * kFwdThreads + tid]);
+        const f2 x = mul2(bc2(dl), a2s[q * CT + tid]);
         const f2 a = linear ? x : mk2(ex2(x.x), ex2(x.y));
         const f2 Bv = *reinterpret_cast<const f2*>(&bcf[bc_index<NS, LBS_BC_IL>(t, 0, 2 * q)]);
         H[q] = fma2(a, H[q], mul2(bc2(du), Bv));
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
   if (!linear) {
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-      const f2 x = mul2(bc2(dsum), a2s[q * kFwdThreads + tid]);
+      const f2 x = mul2(bc2(dsum), a2s[q * CT + tid]);
       P[q] = mk2(ex2(x.x), ex2(x.y));
     }
   }
@@ -736,36 +736,117 @@ __global__ void __launch_bounds__(kFwdThreads) segment_state_kernel(FwdParams p)
 }
 
 // ---------------------------------------------------------------------------
+// Pass 2 of the sequence split: for every lane (b, e, state pair) the states
+// entering segments 1..S-1, h_{s+1} = P_s h_s + H_s with h_0 = 0, written into
+// the H slot of segment s.  One warp per lane, a parallel scan of the affine
+// maps (P, H) (core.py:48-55 combine): each thread composes up to 16
+// consecutive segment maps (loads all in flight), the warp scans the 32
+// composed maps with shuffles, then each thread replays its segments from the
+// scanned carry-in and stores the entering states.  Rounds of 512 segments
+// carry the state across.
+template <int NS>
+__global__ void __launch_bounds__(128) segment_prefix_kernel(FwdParams p) {
+  constexpr int NP = NS / 2;
+  constexpr int K = 16;  // segments per thread per round
+  const long long wid = ((long long)blockIdx.x * 128 + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  const long long total = (long long)p.Bt * p.E * NP;
+  if (wid >= total) return;
+  const int q = (int)(wid % NP);
+  const int e = (int)((wid / NP) % p.E);
+  const int b = (int)(wid / ((long long)NP * p.E));
+  f2* base = reinterpret_cast<f2*>(p.seg_agg) + (((long long)b * p.n_seg) * p.E + e) * NS;
+  const long long sstride = (long long)p.E * NS;  // f2 units per segment
+  const int nmaps = p.n_seg - 1;                  // aggregates of segments 0..S-2
+  f2 carry = mk2(0.f, 0.f);
+  for (int r0 = 0; r0 < nmaps; r0 += 32 * K) {
+    const int s0 = r0 + lane * K;
+    f2 P[K], H[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (s0 + k < nmaps) {
+        P[k] = base[(s0 + k) * sstride + q];
+        H[k] = base[(s0 + k) * sstride + NP + q];
+      } else {
+        P[k] = mk2(1.f, 1.f);
+        H[k] = mk2(0.f, 0.f);
+      }
+    }
+    // compose this thread's maps: x -> Pc x + Hc
+    f2 Pc = mk2(1.f, 1.f), Hc = mk2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      Hc = fma2(P[k], Hc, H[k]);
+      Pc = mul2(P[k], Pc);
+    }
+    // inclusive warp scan of the composed maps (earlier lanes applied first)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float px = __shfl_up_sync(0xffffffffu, Pc.x, o), py = __shfl_up_sync(0xffffffffu, Pc.y, o);
+      const float hx = __shfl_up_sync(0xffffffffu, Hc.x, o), hy = __shfl_up_sync(0xffffffffu, Hc.y, o);
+      if (lane >= o) {
+        Hc = fma2(Pc, mk2(hx, hy), Hc);
+        Pc = mul2(Pc, mk2(px, py));
+      }
+    }
+    // exclusive prefix applied to the round's carry-in = state entering segment s0
+    float epx = __shfl_up_sync(0xffffffffu, Pc.x, 1), epy = __shfl_up_sync(0xffffffffu, Pc.y, 1);
+    float ehx = __shfl_up_sync(0xffffffffu, Hc.x, 1), ehy = __shfl_up_sync(0xffffffffu, Hc.y, 1);
+    if (lane == 0) { epx = epy = 1.f; ehx = ehy = 0.f; }
+    f2 h = fma2(mk2(epx, epy), carry, mk2(ehx, ehy));
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (s0 + k < nmaps) {
+        h = fma2(P[k], h, H[k]);
+        base[(s0 + k) * sstride + NP + q] = h;  // state entering segment s0 + k + 1
+      }
+    }
+    // carry = state after the round's last map (inclusive scan of lane 31 applied to carry)
+    const f2 last = fma2(Pc, carry, Hc);
+    carry = mk2(__shfl_sync(0xffffffffu, last.x, 31), __shfl_sync(0xffffffffu, last.y, 31));
+  }
+}
+
 // launcher
 
-template <typename Tio, typename Tbc, int NS, int MT, bool kVec>
+template <typename Tio, typename Tbc, int NS, int MT, bool kVec, int CT>
 inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
-  const size_t smem = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT)>::total;
-  dim3 block(kFwdThreads);
+  const size_t smem = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT), CT>::total;
+  dim3 block(CT);
   if (p.n_seg > 1) {
-    const size_t smem1 = FwdSmem<Tio, Tbc, NS, LBS_FWD_CL>::total;
-    auto k1 = segment_state_kernel<Tio, Tbc, NS, kVec>;
+    const size_t smem1 = FwdSmem<Tio, Tbc, NS, LBS_FWD_CL, CT>::total;
+    auto k1 = segment_state_kernel<Tio, Tbc, NS, kVec, CT>;
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-    dim3 g1((p.E + kFwdThreads - 1) / kFwdThreads, p.Bt, p.n_seg - 1);
+    dim3 g1((p.E + CT - 1) / CT, p.Bt, p.n_seg - 1);
     k1<<<g1, block, smem1, st>>>(p);
+    const long long lanes = (long long)p.Bt * p.E * (NS / 2);  // one warp each
+    segment_prefix_kernel<NS><<<(unsigned)((lanes * 32 + 127) / 128), 128, 0, st>>>(p);
   }
-  dim3 grid((p.E + kFwdThreads - 1) / kFwdThreads, p.Bt, p.n_seg);
+  dim3 grid((p.E + CT - 1) / CT, p.Bt, p.n_seg);
   // LBS_FLAG_ACCUM is instantiated for the forward-only scan (the global-bidir
   // baseline's second sweep); the C ABI rejects ACCUM together with LB
-  auto k = (p.flags & LBS_FLAG_LB)      ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec>
-           : (p.flags & LBS_FLAG_ACCUM) ? fwd_kernel<Tio, Tbc, NS, MT, false, kVec, true>
-                                        : fwd_kernel<Tio, Tbc, NS, MT, false, kVec>;
+  auto k = (p.flags & LBS_FLAG_LB)      ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec, false, CT>
+           : (p.flags & LBS_FLAG_ACCUM) ? fwd_kernel<Tio, Tbc, NS, MT, false, kVec, true, CT>
+                                        : fwd_kernel<Tio, Tbc, NS, MT, false, kVec, false, CT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, block, smem, st>>>(p);
   return cudaGetLastError();
 }
 
+// CTA width: 128 channels, or 64 when channels are scarce (p.cta == 64: no idle
+// threads for E <= 64, finer load balance and twice the resident segments)
+template <typename Tio, typename Tbc, int NS, int MT, bool kVec>
+inline cudaError_t launch_fwd_c(const FwdParams& p, cudaStream_t st) {
+  if (p.cta == 64) return launch_fwd_t<Tio, Tbc, NS, MT, kVec, 64>(p, st);
+  return launch_fwd_t<Tio, Tbc, NS, MT, kVec, kFwdThreads>(p, st);
+}
+
 template <typename Tio, typename Tbc, int NS, bool kVec>
 inline cudaError_t launch_fwd_m(const FwdParams& p, cudaStream_t st) {
-  if (p.m <= 1) return launch_fwd_t<Tio, Tbc, NS, 1, kVec>(p, st);
-  if (p.m <= 4) return launch_fwd_t<Tio, Tbc, NS, 4, kVec>(p, st);
-  if (p.m <= 8) return launch_fwd_t<Tio, Tbc, NS, 8, kVec>(p, st);
-  return launch_fwd_t<Tio, Tbc, NS, 16, kVec>(p, st);
+  if (p.m <= 1) return launch_fwd_c<Tio, Tbc, NS, 1, kVec>(p, st);
+  if (p.m <= 4) return launch_fwd_c<Tio, Tbc, NS, 4, kVec>(p, st);
+  if (p.m <= 8) return launch_fwd_c<Tio, Tbc, NS, 8, kVec>(p, st);
+  return launch_fwd_c<Tio, Tbc, NS, 16, kVec>(p, st);
 }
 
 template <typename Tio, typename Tbc, bool kVec>

@@ -314,3 +314,15 @@ def test_global_bidir_fused(dtype):
     tol = TOL_F32 if dtype == torch.float32 else TOL_BF16
     assert O.max_rel_err(out.float().cpu().numpy(), rf + rb) <= tol
     assert O.max_rel_err(h.cpu().numpy(), hf + hb) <= tol
+
+
+@pytest.mark.parametrize("S", [40, 700])
+def test_many_segments_prefix(S):
+    """Sequence split into many segments (more than one 512-segment round of the
+    parallel prefix): equals the oracle."""
+    inp = op_inputs(60 + S, 1, 16 * S + 5, 8, 16)
+    for reverse in (False, True):
+        got, hf = run_gpu(inp, window=16, reverse=reverse, return_last_state=True, seg_hint=S)
+        ref, rhf = O.lbm_selective_scan(**inp, window=16, reverse=reverse, return_last_state=True)
+        assert O.max_rel_err(got, ref) <= TOL_F32
+        assert O.max_rel_err(hf, rhf) <= TOL_F32
