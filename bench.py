@@ -204,7 +204,8 @@ def measure_ops(peak, iters=10):
     names = {"cfg1": "configs[0] op fwd fp32 B=2 E=192 L=197", "cfg2": "configs[1] LBVim-Ti layer scan bf16 B=256 E=384",
              "cfg3": "configs[2] LBVim-S scan fp32 B=128 E=768 fwd+bwd", "cfg4": "configs[3] LBVim-S 1024^2 layer scan bf16 "
              "B=32 L=4096 E=768", "cfg5": "configs[4] MIL bag fp32 B=1 L=100k E=512 (1 GPU)",
-             "cfg5s": "configs[4] one 8-way channel shard (E=64)"}
+             "cfg5s": "configs[4] one 8-way channel shard (E=64)",
+             "cfg3s": "configs[2] per-GPU batch shard at 8 GPUs (B=16) fwd+bwd"}
     res = {}
     for name, (Bt, L, E, N, M, io, bc) in CFGS.items():
         x = make(Bt, L, E, N, io, bc)
@@ -220,7 +221,7 @@ def measure_ops(peak, iters=10):
              "global_bidir_ms": bi_ms, "lb_over_bidir": (lb_ms / bi_ms) if bi_ms else None,
              "lb_over_fwd": lb_ms / fw_ms, "bytes": nb, "gbs": nb / lb_ms / 1e6, "frac": nb / lb_ms / 1e6 / peak,
              "lanes_per_s": Bt * L * E * N / lb_ms * 1e3}
-        if name == "cfg3":
+        if name in ("cfg3", "cfg3s"):
             dout = torch.randn(Bt, L, E, device="cuda").to(io)
             _, ck = lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True)
             nbb = bwd_alg_bytes(Bt, L, E, N, s_io, s_bc, s_io)
