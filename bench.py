@@ -167,8 +167,8 @@ def cpu_reference_run(steps, warmup, batch=CPU_SAMPLE_BATCH):
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    steps = max(1, min(args.steps, 8))
-    warm = max(1, min(args.warmup, 1))
+    steps = max(1, min(args.steps, 20))  # ~0.4 s per 2-image step on 16 cores
+    warm = max(1, min(args.warmup, 5))
     r = cpu_reference_run(steps, warm)
     line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
             "warmup": warm, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
