@@ -168,10 +168,58 @@ def bidir_cases():
     return out
 
 
-def main():
+def cost_cases():
+    """costmodel.count_scan_cost / count_model_cost / reports_to_csv / format_table
+    (costmodel.py:90-227) and the counters the engine tallies at run time
+    (engine.py:290), which the reference asserts equal to the closed form."""
+    from lbscan import costmodel
+
+    out = {}
+    dims, counters, variants = [], [], []
+    for variant in ("forward", "lbm", "global_bidir"):
+        for (B, L, E, N, M) in ((1, 1, 1, 1, 1), (2, 300, 4, 8, 8), (1, 100, 3, 4, 1), (1, 64, 2, 4, 4),
+                                (2, 197, 3, 16, 8), (1, 4096, 2, 16, 16), (3, 257, 5, 4, 3), (1, 129, 2, 2, 16),
+                                (256, 197, 384, 16, 8), (1, 100000, 512, 16, 16)):
+            r = costmodel.count_scan_cost(variant, B, L, E, N, M)
+            dims.append((B, L, E, N, M))
+            variants.append(variant)
+            counters.append([r.flops, r.hbm_reads, r.hbm_writes, r.tile_exchanges, r.register_ops])
+    out["scan_dims"] = np.array(dims, dtype=np.int64)
+    out["scan_variants"] = np.array(variants)
+    out["scan_counters"] = np.array(counters, dtype=np.int64)
+    # engine-tallied counters on a small run (engine.py:290 vs the closed form)
+    p = random_scan_params(seeded_rng(3), 2, 37, 3, 4)
+    plan = engine.TilePlan.for_length(37, 8)
+    tallied = []
+    for fn in (engine.forward_scan_par, engine.lbm_scan_par):
+        c = fn(p.abar, p.bx, p.c, p.dx, plan).cost
+        tallied.append([c.flops, c.hbm_reads, c.hbm_writes, c.tile_exchanges, c.register_ops])
+    out["engine_counters"] = np.array(tallied, dtype=np.int64)
+    cfgs = [dict(), dict(inner_dim=64), dict(head="map", class_token="head"),
+            dict(image_size=224, patch_size=16, in_channels=3, embed_dim=192, inner_dim=384, state_dim=16,
+                 depth=24, class_token="middle", num_classes=1000),
+            dict(scan_variant="forward", tile_len=4)]
+    mc = []
+    for kw in cfgs:
+        r = costmodel.count_model_cost(model.ModelConfig(**kw))
+        mc.append([r.flops, r.hbm_reads, r.hbm_writes, r.tile_exchanges, r.register_ops])
+    out["model_cfgs"] = np.array([repr(kw) for kw in cfgs])
+    out["model_counters"] = np.array(mc, dtype=np.int64)
+    reps = [costmodel.count_scan_cost(v, 2, 300, 4, 8, 8) for v in ("forward", "lbm", "global_bidir")]
+    out["csv"] = np.array(costmodel.reports_to_csv(reps))
+    out["table"] = np.array(costmodel.format_table(reps))
+    return out
+
+
+CASES = (("scan_grid", scan_grid), ("scan_grads", scan_grads), ("block", block_cases),
+         ("conv", conv_cases), ("model", model_cases), ("bidir", bidir_cases), ("costs", cost_cases))
+
+
+def main(only=()):
     os.makedirs(OUT, exist_ok=True)
-    for name, fn in (("scan_grid", scan_grid), ("scan_grads", scan_grads), ("block", block_cases),
-                     ("conv", conv_cases), ("model", model_cases), ("bidir", bidir_cases)):
+    for name, fn in CASES:
+        if only and name not in only:
+            continue
         data = fn()
         path = os.path.join(OUT, f"{name}.npz")
         np.savez_compressed(path, **data)
@@ -179,4 +227,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]))  # e.g. python oracle/gen_golden.py costs

@@ -50,6 +50,9 @@ void plan_fwd(const lbs_scan_fwd_args* a, int* cta, int* n_seg, int* seg_len) {
   const int64_t L = a->seqlen, m = a->window < a->seqlen ? a->window : a->seqlen;
   const int64_t ctas128 = ((a->dim + 127) / 128) * a->batch;
   *cta = (a->dim <= 64 || ctas128 < 2 * kNumSMs) ? 64 : 128;
+#ifdef LBS_FORCE_CTA
+  *cta = LBS_FORCE_CTA;  // dev experiments only
+#endif
   const int64_t warps = ((a->dim + 31) / 32) * a->batch;
   int64_t S = 1;
   if (a->seg_hint > 0) {

@@ -1,5 +1,6 @@
 // Shared device helpers for the lbscan_b200 kernels (sm_100a only).
 #pragma once
+#include <type_traits>
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -81,6 +82,26 @@ __device__ __forceinline__ float softplus_f(float x) {
 // sigmoid(x) = 1 / (1 + e^-x); silu(x) = x * sigmoid(x)  (nn.py:16-26)
 __device__ __forceinline__ float sigmoid_f(float x) { return rcp(1.0f + ex2(-x * kLog2e)); }
 __device__ __forceinline__ float silu_f(float x) { return x * sigmoid_f(x); }
+__device__ __forceinline__ float tanh_approx(float x) {
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+#ifndef LBS_SILU_TANH
+#define LBS_SILU_TANH 0
+#endif
+// SiLU for a value that is stored as T: for 16-bit outputs sigmoid(x) =
+// 0.5 + 0.5 tanh(x/2) with MUFU.TANH (one MUFU instead of EX2 + RCP; its
+// ~2^-11 relative error is 8x below the bf16 store's rounding), else silu_f.
+template <typename T>
+__device__ __forceinline__ float silu_out(float x) {
+  if constexpr (LBS_SILU_TANH && sizeof(T) == 2) {
+    const float hx = 0.5f * x;
+    return fmaf(hx, tanh_approx(hx), hx);
+  } else {
+    return silu_f(x);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // typed loads / stores (fp32 compute, io in fp32 / bf16 / fp16)
@@ -98,6 +119,13 @@ __device__ __forceinline__ float ld<__half>(const __half* p) { return __half2flo
 __device__ __forceinline__ float to_f(float x) { return x; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
 __device__ __forceinline__ float to_f(__half x) { return __half2float(x); }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float v) {
+  if constexpr (sizeof(T) == 4) return v;
+  else if constexpr (std::is_same<T, __nv_bfloat16>::value) return __float2bfloat16_rn(v);
+  else return __float2half_rn(v);
+}
 
 template <typename T>
 __device__ __forceinline__ void st(T* p, float v);

@@ -258,6 +258,9 @@ struct TileOut {
 #define LBS_DBG_NOSTORE 0
 #endif
 
+#ifndef LBS_SP_HOIST
+#define LBS_SP_HOIST 1
+#endif
 #ifndef LBS_QUNROLL16
 #define LBS_QUNROLL16 2  // the same for 16-step tiles
 #endif
@@ -339,12 +342,23 @@ __device__ __forceinline__ void pair_tile(f2& hq, const f2 A2, int q, const floa
     f2 s = mk2(0.f, 0.f);
 #pragma unroll
     for (int j = MT - 1; j >= 0; --j) {
-      if (kFull ? (j == MT - 1) : (j == r - 1)) {
-        s = binj(j);
-      } else if (kFull || j < r - 1) {
+      if (kFull) {
+        if (j == MT - 1) {
+          s = binj(j);
+        } else {
+          const f2 rr = mul2(a[j], s);
+          yacc[j] = fma2(cinj(j), rr, yacc[j]);
+          s = add2(rr, binj(j));
+        }
+      } else if (j < r) {
+        // ragged tile: selects on the (runtime) tile end instead of a branch
+        // chain, which the compiler turns into a local-memory lookup b[r-1]
+        const bool end = j == r - 1;
         const f2 rr = mul2(a[j], s);
-        yacc[j] = fma2(cinj(j), rr, yacc[j]);
-        s = add2(rr, binj(j));
+        if (!end) yacc[j] = fma2(cinj(j), rr, yacc[j]);
+        const f2 bj = binj(j);
+        const f2 sn = add2(rr, bj);
+        s = end ? bj : sn;
       }
     }
   }
@@ -413,13 +427,19 @@ struct StateStore {
   }
 };
 
+// kFull: a whole tile (r == MT) through the MT-step unrolled code; else a
+// ragged tile (once per segment).  Measured: an extra unrolled instantiation
+// for ragged tiles (masked steps) costs 4-10 % on every config even where it
+// never runs, and so does a runtime step count inside the full-tile code
+// (ragged tiles padded with delta = -inf) -- r must stay a compile-time MT here.
 template <typename Tio, int NS, int MT, bool kLB, bool kFull, int QU, bool kRegs, bool kAccum = false,
           int CT = kFwdThreads>
 __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const Tio* sz,
                                              const float* bcf, const f2* a2s, StateStore<NS / 2, kRegs, CT>& h,
-                                             int t0, int r, float bias, bool softplus, bool linear,
+                                             int t0, int r_, float bias, bool softplus, bool linear,
                                              const TileOut& o) {
   constexpr int NP = NS / 2;
+  const int r = kFull ? MT : r_;
   const int tid = threadIdx.x;
   float dl[MT], du[MT];
   f2 yacc[MT];
@@ -429,19 +449,33 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
   if (kAccum && o.active) {
     const Tio* opp = static_cast<const Tio*>(o.op);
 #pragma unroll
-    for (int j = 0; j < MT; ++j) prev[j] = (kFull || j < r) ? to_f(opp[(long long)(o.c + t0 + j) * o.step]) : 0.f;
+    for (int j = 0; j < MT; ++j) prev[j] = (j < r) ? to_f(opp[(long long)(o.c + t0 + j) * o.step]) : 0.f;
   }
+  float uv[MT];
 #pragma unroll
   for (int j = 0; j < MT; ++j) {
     const bool on = kFull || j < r;
-    float d = on ? to_f(sd[(t0 + j) * CT + tid]) + bias : 0.f;
-    const float uv = on ? to_f(su[(t0 + j) * CT + tid]) : 0.f;
+    dl[j] = on ? to_f(sd[(t0 + j) * CT + tid]) + bias : 0.f;
+    uv[j] = on ? to_f(su[(t0 + j) * CT + tid]) : 0.f;
+  }
 #if !LBS_DBG_NOSOFTPLUS
-    if (softplus) d = softplus_f(d);
+#if LBS_SP_HOIST
+  // one uniform branch per tile: the MT softplus chains (EX2 -> LG2) are
+  // independent and interleave
+  if (softplus) {
+#pragma unroll
+    for (int j = 0; j < MT; ++j) dl[j] = softplus_f(dl[j]);
+  }
+#else
+#pragma unroll
+  for (int j = 0; j < MT; ++j)
+    if (softplus) dl[j] = softplus_f(dl[j]);
 #endif
-    dl[j] = d;
-    du[j] = d * uv;
-    yacc[j] = mk2(o.Dv * uv, 0.f);  // D-skip folded into the accumulator
+#endif
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    du[j] = dl[j] * uv[j];
+    yacc[j] = mk2(o.Dv * uv[j], 0.f);  // D-skip folded into the accumulator
   }
   if constexpr (kRegs) {
 #pragma unroll
@@ -479,20 +513,20 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
     }
   }
   if (o.active) {
-    Tio* op = static_cast<Tio*>(o.op);
+    Tio* dst = static_cast<Tio*>(o.op) + (long long)(o.c + t0) * o.step;
 #pragma unroll
     for (int j = 0; j < MT; ++j) {
-      if (kFull || j < r) {
+      if (j < r) {
         float y = yacc[j].x + yacc[j].y;
 #if LBS_DBG_NOSTORE  // ablation only
-        if (y == 1234.5f) st<Tio>(op + (long long)(o.c + t0 + j) * o.step, y);
+        if (y == 1234.5f) st<Tio>(dst, y);
 #else
-        if (o.has_z) y *= silu_f(to_f(sz[(t0 + j) * CT + tid]));
-        Tio* dst = op + (long long)(o.c + t0 + j) * o.step;
+        if (o.has_z) y *= silu_out<Tio>(to_f(sz[(t0 + j) * CT + tid]));
         if constexpr (kAccum) y += prev[j];
         st<Tio>(dst, y);
 #endif
       }
+      dst += o.step;
     }
   }
 }

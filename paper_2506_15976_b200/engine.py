@@ -20,13 +20,16 @@ import numpy as np
 import torch
 
 from . import _lib
+from .costmodel import count_scan_cost
 from .errors import ShapeError
 from .tiling import TilePlan, select_tile_len  # noqa: F401  (re-export, engine.py:54-85)
 
 
 @dataclass
 class ScanOutput:
-    """Mirror of core.OracleOutput (core.py:120-128) without cost counters."""
+    """Mirror of core.OracleOutput (core.py:120-128); ``cost`` carries the
+    reference's counters for the call (costmodel.count_scan_cost, which the
+    reference engine's run-time tallies equal, engine.py:290)."""
 
     y: object
     h_final: object
@@ -39,7 +42,7 @@ def _to_dev(x, dtype):
     return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda"), False
 
 
-def _run(abar, bx, c, dx, plan, workers, do_backward, reverse):
+def _run(abar, bx, c, dx, plan, workers, do_backward, reverse, variant):
     if workers < 1:
         raise ShapeError(f"workers must be >= 1, got {workers}")  # engine.py:239-242
     is_t = isinstance(abar, torch.Tensor)
@@ -67,28 +70,32 @@ def _run(abar, bx, c, dx, plan, workers, do_backward, reverse):
     a.y, a.h_final = y.data_ptr(), hf.data_ptr()
     rc = _lib.lib().lbs_prediscretized_fwd(ctypes.byref(a), torch.cuda.current_stream().cuda_stream)
     _lib.check(rc, "lbm_scan_par")
+    cost = count_scan_cost(variant, B, L, E, N, plan.tile_len)
+    if variant == "global_bidir":  # one of the two sweeps (engine.py:316-326)
+        cost = count_scan_cost("forward", B, L, E, N, plan.tile_len)
+        cost.variant = variant
     if is_t:
-        return ScanOutput(y=y, h_final=hf)
-    return ScanOutput(y=y.cpu().numpy(), h_final=hf.cpu().numpy())
+        return ScanOutput(y=y, h_final=hf, cost=cost)
+    return ScanOutput(y=y.cpu().numpy(), h_final=hf.cpu().numpy(), cost=cost)
 
 
 def forward_scan_par(abar, bx, c, dx, plan: TilePlan, workers: int = 1) -> ScanOutput:
     """engine.py:294-296."""
-    return _run(abar, bx, c, dx, plan, workers, False, False)
+    return _run(abar, bx, c, dx, plan, workers, False, False, "forward")
 
 
 def lbm_scan_par(abar, bx, c, dx, plan: TilePlan, workers: int = 1) -> ScanOutput:
     """engine.py:299-302."""
-    return _run(abar, bx, c, dx, plan, workers, True, False)
+    return _run(abar, bx, c, dx, plan, workers, True, False, "lbm")
 
 
 def lbm_scan_par_reverse(abar, bx, c, dx, plan: TilePlan, workers: int = 1) -> ScanOutput:
     """engine._run(..., do_backward=True, reverse=True) (engine.py:265-291, 133, 183)."""
-    return _run(abar, bx, c, dx, plan, workers, True, True)
+    return _run(abar, bx, c, dx, plan, workers, True, True, "lbm")
 
 
 def global_bidir_par(params_f, params_b, plan: TilePlan, workers: int = 1) -> ScanOutput:
     """engine.py:305-327: two full sweeps (the second flip-on-load), summed."""
-    f = _run(*params_f, plan, workers, False, False)
-    b = _run(*params_b, plan, workers, False, True)
-    return ScanOutput(y=f.y + b.y, h_final=f.h_final + b.h_final)
+    f = _run(*params_f, plan, workers, False, False, "global_bidir")
+    b = _run(*params_b, plan, workers, False, True, "global_bidir")
+    return ScanOutput(y=f.y + b.y, h_final=f.h_final + b.h_final, cost=f.cost + b.cost)
