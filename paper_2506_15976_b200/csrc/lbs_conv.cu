@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kConvThreads) conv_fwd_kernel(ConvParams p) {
 // loads issued before use.  Requires E % V == 0, unit channel stride and 16-byte
 // aligned rows (checked by the launcher).
 #ifndef LBS_CONV_SMEM
-#define LBS_CONV_SMEM 1
+#define LBS_CONV_SMEM 2  // 2: tile kernel (vector in/out), 1: smem-in kernel, 0: register kernels
 #endif
 #ifndef LBS_CONV_CHUNK
 #define LBS_CONV_CHUNK 16
@@ -244,6 +244,86 @@ __global__ void __launch_bounds__(kConvTileE) conv_fwd_smem_kernel(ConvParams p)
   }
 }
 
+// Tile-staged forward (default for 16-byte aligned rows): a 128-thread CTA owns
+// (b, kConvTT steps, 128 channels).  The (kConvTT + K - 1) input rows arrive by
+// cp.async 16-byte pieces, each thread sweeps its channel through shared memory
+// (K-1 history in registers) into an output tile, and the tile leaves as
+// coalesced 16-byte stores -- every HBM access is a whole 16-byte piece.
+// Flip-on-load: logical row l is physical L-1-l for both the input and output.
+constexpr int kConvTT = 32;
+constexpr int kConvTE = 128;
+
+template <typename T, int KW>
+__global__ void __launch_bounds__(kConvTE) conv_fwd_tile_kernel(ConvParams p) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int ROWS = kConvTT + KW - 1;
+  __shared__ __align__(16) T xin[ROWS][kConvTE];
+  __shared__ __align__(16) T yout[kConvTT][kConvTE];
+  const int e0 = blockIdx.x * kConvTE;
+  const int l0 = blockIdx.y * kConvTT;
+  const int b = blockIdx.z;
+  const int L = p.L;
+  const int EC = min(kConvTE, p.E - e0);
+  const int TT = min(kConvTT, L - l0);
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  const int ppr = EC / V;  // 16-byte pieces per row
+  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
+  for (int i = threadIdx.x; i < ROWS * ppr; i += kConvTE) {
+    const int r = i / ppr, pc = i - r * ppr;
+    const int l = l0 - (KW - 1) + r;
+    T* dst = &xin[r][pc * V];
+    if (l >= 0 && l < L) {
+      cp_async16_conv(dst, xb + (long long)(rev ? L - 1 - l : l) * p.x.s1 + pc * V);
+    } else {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c < EC) {
+    const int e = e0 + c;
+    float w[KW];
+#pragma unroll
+    for (int q = 0; q < KW; ++q) w[q] = q < p.K ? p.w[(long long)e * p.K + q] : 0.f;
+    const float bias = p.bias ? p.bias[e] : 0.f;
+    float hist[KW];  // hist[q] = x[l - q]
+#pragma unroll
+    for (int q = 1; q < KW; ++q) hist[q] = to_f(xin[KW - 1 - q][c]);
+    if (TT == kConvTT) {
+#pragma unroll 8
+      for (int j = 0; j < kConvTT; ++j) {
+        hist[0] = to_f(xin[KW - 1 + j][c]);
+        float acc = bias;
+#pragma unroll
+        for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], hist[q], acc);
+        yout[j][c] = from_f<T>(act ? silu_f(acc) : acc);
+#pragma unroll
+        for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
+      }
+    } else {
+      for (int j = 0; j < TT; ++j) {
+        hist[0] = to_f(xin[KW - 1 + j][c]);
+        float acc = bias;
+#pragma unroll
+        for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], hist[q], acc);
+        yout[j][c] = from_f<T>(act ? silu_f(acc) : acc);
+#pragma unroll
+        for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
+      }
+    }
+  }
+  __syncthreads();
+  T* ob = static_cast<T*>(p.out) + (long long)b * p.so0 + e0;
+  for (int i = threadIdx.x; i < TT * ppr; i += kConvTE) {
+    const int j = i / ppr, pc = i - j * ppr;
+    const int l = l0 + j;
+    *reinterpret_cast<uint4*>(ob + (long long)(rev ? L - 1 - l : l) * p.so1 + pc * V) =
+        *reinterpret_cast<const uint4*>(&yout[j][pc * V]);
+  }
+}
+
 template <typename T, int KW>
 __global__ void __launch_bounds__(kConvThreads) conv_bwd_kernel(ConvParams p) {
   const int e = blockIdx.x * kConvThreads + threadIdx.x;
@@ -332,6 +412,12 @@ static bool conv_vec_ok(const ConvParams& p) {
 
 template <typename T>
 static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
+  if (conv_vec_ok<T>(p) && LBS_CONV_SMEM == 2) {
+    dim3 grid((p.E + kConvTE - 1) / kConvTE, (p.L + kConvTT - 1) / kConvTT, p.Bt);
+    if (p.K <= 4) conv_fwd_tile_kernel<T, 4><<<grid, kConvTE, 0, st>>>(p);
+    else conv_fwd_tile_kernel<T, kMaxWidth><<<grid, kConvTE, 0, st>>>(p);
+    return cudaGetLastError();
+  }
   if (conv_vec_ok<T>(p) && LBS_CONV_SMEM) {
     dim3 grid((p.E + kConvTileE - 1) / kConvTileE, (p.L + kConvTileT - 1) / kConvTileT, p.Bt);
     if (p.K <= 4) conv_fwd_smem_kernel<T, 4><<<grid, kConvTileE, 0, st>>>(p);

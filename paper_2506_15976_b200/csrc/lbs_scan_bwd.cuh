@@ -171,20 +171,32 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
   const int clen = x.clen;
   float dl[KT], dlu[KT], gy[KT];
   f2 Y[KT], Pacc[KT], S[KT];
+  float uvs[KT];
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
     const bool on = kFull || j < clen;
-    float d = on ? to_f(sd[j * kBwdThreads + tid]) + x.bias : 0.f;
-    const float uv = on ? to_f(su[j * kBwdThreads + tid]) : 0.f;
-    if (x.softplus) d = softplus_f(d);
-    float g = (on && x.active) ? to_f(sg[j * kBwdThreads + tid]) : 0.f;
-    if (x.has_z && on) g *= silu_f(to_f(sz[j * kBwdThreads + tid]));
-    dl[j] = on ? d : 0.f;
-    dlu[j] = on ? d * uv : 0.f;
-    gy[j] = g;
+    dl[j] = on ? to_f(sd[j * kBwdThreads + tid]) + x.bias : 0.f;
+    uvs[j] = on ? to_f(su[j * kBwdThreads + tid]) : 0.f;
+    gy[j] = (on && x.active) ? to_f(sg[j * kBwdThreads + tid]) : 0.f;
     Y[j] = mk2(0.f, 0.f);
     Pacc[j] = mk2(0.f, 0.f);
     S[j] = mk2(0.f, 0.f);
+  }
+  // one uniform branch per chunk for each of softplus and the gate: the
+  // per-step MUFU chains are independent and interleave
+  if (x.softplus) {
+#pragma unroll
+    for (int j = 0; j < KT; ++j) dl[j] = softplus_f(dl[j]);
+  }
+  if (x.has_z) {
+#pragma unroll
+    for (int j = 0; j < KT; ++j)
+      if (kFull || j < clen) gy[j] *= silu_f(to_f(sz[j * kBwdThreads + tid]));
+  }
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    if (!(kFull || j < clen)) dl[j] = 0.f;
+    dlu[j] = dl[j] * uvs[j];
   }
   const int jlast = kFull ? KT - 1 : clen - 1;
 
@@ -310,10 +322,13 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
 
   // ---- per-step outputs: du, ddelta, dz
   if (x.active) {
+    Tio* dupj = dup + (long long)x.c * sdu;
+    Tio* ddpj = ddp + (long long)x.c * sdd;
+    Tio* dzpj = dzp + (long long)x.c * sdz;
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
       if (kFull || j < clen) {
-        const float uv = to_f(su[j * kBwdThreads + tid]);
+        const float uv = uvs[j];
         const float s = S[j].x + S[j].y;
         const float duv = x.Dv * gy[j] + dl[j] * s;
         const float pp = (Pacc[j].x + Pacc[j].y) * (x.linear ? 1.f : kLn2);
@@ -322,17 +337,19 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
         const float ddv = x.softplus ? ddl * sigmoid_f(dpre) : ddl;
         dbias_acc += ddv;
         dD_acc += gy[j] * uv;
-        const long long t = x.c + j;
-        st<Tio>(dup + t * sdu, duv);
-        st<Tio>(ddp + t * sdd, ddv);
+        st<Tio>(dupj, duv);
+        st<Tio>(ddpj, ddv);
         if (x.has_z) {
           const float y = Y[j].x + Y[j].y + x.Dv * uv;
           const float zv = to_f(sz[j * kBwdThreads + tid]);
           const float sgm = sigmoid_f(zv);
           const float go = to_f(sg[j * kBwdThreads + tid]);
-          st<Tio>(dzp + t * sdz, go * y * sgm * (1.f + zv * (1.f - sgm)));
+          st<Tio>(dzpj, go * y * sgm * (1.f + zv * (1.f - sgm)));
         }
       }
+      dupj += sdu;
+      ddpj += sdd;
+      dzpj += sdz;
     }
   }
 }
