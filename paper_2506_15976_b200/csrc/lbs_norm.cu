@@ -24,6 +24,20 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const T* __restrict__ x, 
       if (row0 + r < rows && c0 < D) raw[r][k] = *reinterpret_cast<const uint4*>(x + (row0 + r) * sx + c0);
       else raw[r][k] = make_uint4(0, 0, 0, 0);
     }
+  // this lane's scale entries, loaded once per warp (16-byte loads)
+  float sc[VPL][EPV];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c0 = (lane + 32 * k) * EPV;
+#pragma unroll
+    for (int i = 0; i < EPV; i += 4) {
+      const float4 s4 = c0 < D ? __ldg(reinterpret_cast<const float4*>(scale + c0 + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      sc[k][i] = s4.x;
+      sc[k][i + 1] = s4.y;
+      sc[k][i + 2] = s4.z;
+      sc[k][i + 3] = s4.w;
+    }
+  }
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
     if (row0 + r >= rows) break;
@@ -50,7 +64,7 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const T* __restrict__ x, 
         T* e = reinterpret_cast<T*>(&o4);
 #pragma unroll
         for (int i = 0; i < EPV; ++i) {
-          const float y = v[k][i] * inv * __ldg(scale + c0 + i);
+          const float y = v[k][i] * inv * sc[k][i];
           if constexpr (sizeof(T) == 4) e[i] = y;
           else e[i] = __float2bfloat16_rn(y);
         }
@@ -88,13 +102,13 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
   T* o = static_cast<T*>(p.out);
   const bool vec = p.D % EPV == 0 && (p.sx * (long long)sizeof(T)) % 16 == 0 &&
                    (p.so * (long long)sizeof(T)) % 16 == 0 && reinterpret_cast<uintptr_t>(p.x) % 16 == 0 &&
-                   reinterpret_cast<uintptr_t>(p.out) % 16 == 0 && vpl <= 4;
+                   reinterpret_cast<uintptr_t>(p.out) % 16 == 0 && reinterpret_cast<uintptr_t>(p.scale) % 16 == 0 && vpl <= 4;
   if (!vec) {
     rms_norm_scalar_kernel<T><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
     return cudaGetLastError();
   }
 #ifndef LBS_NORM_RPW
-#define LBS_NORM_RPW 1
+#define LBS_NORM_RPW 1  // rows per warp (2, 4, 8 measured no better)
 #endif
   constexpr int RPW = LBS_NORM_RPW;
   dim3 gridv((unsigned)((p.rows + 8 * RPW - 1) / (8 * RPW)));
