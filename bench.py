@@ -243,7 +243,18 @@ def measure_ops(peak, iters=10):
     ms = time_fn(run, 3, flush)
     res["cfg4_model"] = {"what": "configs[3] LBVim-S 1024^2 patch16 forward, batch 32, bf16, 24 layers, L=4097",
                          "ms_per_batch": ms, "images_per_s": 32 / ms * 1e3}
-    del net, imgs, run, flush
+    del net, imgs, run
+    torch.cuda.empty_cache()
+    # configs[4] as a workload: one MambaMIL-style bag (mil.py) on one GPU, bf16
+    from paper_2506_15976_b200.mil import MILBag, MILConfig, init_mil_params
+    mcfg = MILConfig(d_in=1024, dim=512, state_dim=16, dt_rank=32, num_classes=2)
+    bag = MILBag(mcfg, init_mil_params(mcfg, seed=0, device="cuda"), dtype=torch.bfloat16)
+    X = torch.randn(100000, 1024, generator=g, device="cuda").to(torch.bfloat16)
+    ms = time_fn(lambda: bag(X), 5, flush)
+    res["cfg5_model"] = {"what": "configs[4] MambaMIL-style bag forward (fc 1024->512, RMSNorm, in-proj, conv, "
+                                 "x_proj, LB scan E=512 N=16 M=16, mean pool, head), L=100k, bf16, 1 GPU",
+                         "ms_per_bag": ms, "bags_per_s": 1e3 / ms}
+    del bag, X, flush
     torch.cuda.empty_cache()
     return res
 
