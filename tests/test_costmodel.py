@@ -64,3 +64,33 @@ def test_structure():
 def test_fused_bytes_formula():
     # LBVim-Ti layer scan, bf16 = 158.18 MB
     assert costmodel.fused_scan_bytes(256, 197, 384, 16, 2, 2) == 158182400
+
+
+def test_cli_flops(capsys, tmp_path):
+    from paper_2506_15976_b200 import cli
+
+    cfg = tmp_path / "cfg.txt"
+    cfg.write_text("# LBVim-Ti\nimage_size=224\npatch_size=16\nin_channels=3\nembed_dim=192\ninner_dim=384\n"
+                   "depth=24\nclass_token=middle\ntile_len=auto\nnum_classes=1000\nreverse_between_blocks=1\n")
+    out = tmp_path / "o.csv"
+    assert cli.main(["flops", "--config", str(cfg), "--out", str(out)]) == 0
+    text = capsys.readouterr().out
+    want = list(map(int, G["model_counters"][3]))  # the same config in the golden grid
+    assert str(want[0]) in text and "global_bidir" in text
+    rows = out.read_text().splitlines()
+    assert rows[0] == "variant,flops,hbm_reads,hbm_writes,tile_exchanges,register_ops" and len(rows) == 5
+    bad = tmp_path / "bad.txt"
+    bad.write_text("nope=1\n")
+    assert cli.main(["flops", "--config", str(bad)]) == 1
+
+
+@pytest.mark.gpu
+def test_cli_bench_gpu(capsys):
+    from paper_2506_15976_b200 import cli
+
+    assert cli.main(["bench", "--l", "100", "--m", "8", "--reps", "2", "--ben", "512", "--fused"]) == 0
+    lines = capsys.readouterr().out.splitlines()
+    assert lines[0] == "variant,L,M,workers,median_ns,flops,hbm_elems,tile_exchanges"
+    names = [ln.split(",")[0] for ln in lines[1:] if not ln.startswith("#")]
+    assert names == ["forward", "lbm", "global_bidir", "fused_forward", "fused_lbm"]
+    assert any(ln.startswith("# lbm/forward time ratio") for ln in lines)
