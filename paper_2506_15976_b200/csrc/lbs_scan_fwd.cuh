@@ -261,6 +261,9 @@ struct TileOut {
 #ifndef LBS_SP_HOIST
 #define LBS_SP_HOIST 1
 #endif
+#ifndef LBS_RAGGED_QU
+#define LBS_RAGGED_QU 2  // state pairs per unrolled group in the LB ragged-tile path (-2..4 % vs 1)
+#endif
 #ifndef LBS_QUNROLL16
 #define LBS_QUNROLL16 2  // the same for 16-step tiles
 #endif
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
 #pragma unroll
           for (int q = 0; q < NP; ++q) hp.set(q, h.get(q));
         }
-        tile_compute<Tio, NS, MT, kLB, false, 1, false, kAccum, CT>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, false, (kLB ? LBS_RAGGED_QU : 1), false, kAccum, CT>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
         if constexpr (kRegs) {
 #pragma unroll
           for (int q = 0; q < NP; ++q) h.set(q, hp.get(q));
