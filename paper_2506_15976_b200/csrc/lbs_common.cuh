@@ -80,6 +80,7 @@ __device__ __forceinline__ float softplus_f(float x) {
   return (x < -15.0f) ? t : s;
 }
 // sigmoid(x) = 1 / (1 + e^-x); silu(x) = x * sigmoid(x)  (nn.py:16-26)
+// (a MUFU-free Newton reciprocal measured 1-13 % slower in the scan and the conv)
 __device__ __forceinline__ float sigmoid_f(float x) { return rcp(1.0f + ex2(-x * kLog2e)); }
 __device__ __forceinline__ float silu_f(float x) { return x * sigmoid_f(x); }
 __device__ __forceinline__ float tanh_approx(float x) {

@@ -253,7 +253,10 @@ __global__ void __launch_bounds__(kConvTileE) conv_fwd_smem_kernel(ConvParams p)
 // (K-1 history in registers) into an output tile, and the tile leaves as
 // coalesced 16-byte stores -- every HBM access is a whole 16-byte piece.
 // Flip-on-load: logical row l is physical L-1-l for both the input and output.
-constexpr int kConvTT = 32;
+#ifndef LBS_CONV_TT
+#define LBS_CONV_TT 32
+#endif
+constexpr int kConvTT = LBS_CONV_TT;
 constexpr int kConvTE = 128;
 
 template <typename T, int KW>
