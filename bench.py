@@ -185,6 +185,19 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 # our arm
 
+def xu_roofline(B, L, E, N, ms, clocks):
+    """The binding pipe of the fused scan: MUFU (XU) ops per launch = (N state exps +
+    2 softplus + 2 SiLU) per (b, l, e), against 16 MUFU lanes/clk/SM x 148 SMs at the
+    SM clock sampled during the timed region."""
+    ops = (N + 4) * B * L * E
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    peak = 16 * 148 * mhz * 1e6 / 1e9  # G MUFU ops/s
+    achieved = ops / (ms / 1e3) / 1e9
+    return {"bound": "mufu", "ops_per_launch": ops, "achieved": achieved, "peak": peak,
+            "unit": "Gop/s", "frac": achieved / peak,
+            "peak_source": "16 MUFU.EX2 lanes/clk/SM (measured, tools/micro) x 148 SMs x sampled SM clock"}
+
+
 def scan_alg_bytes(B, L, E, N, s_io, s_bc):
     """s_in*B*L*(3E + 2N) + s_out*B*L*E + 4*(E*N + 2E)."""
     return s_io * B * L * 3 * E + s_bc * B * L * 2 * N + s_io * B * L * E + 4 * (E * N + 2 * E)
@@ -416,7 +429,8 @@ def run_ours(args, rank, world, local_rank):
                          "kernel": "lbs::fwd_kernel (fused discretize + LB scan + D skip + SiLU gate)",
                          "bytes_per_launch": nbytes, "ms_per_launch": scan_ms, "peak_source": peak_src,
                          "share_of_step": scan_share,
-                         "note": "MUFU/issue-bound: 1 ex2 + ~3.5 packed FP32 ops per state-step (DESIGN.md)"},
+                         "note": "MUFU/issue-bound: 1 ex2 + ~3.5 packed FP32 ops per state-step (DESIGN.md)",
+                         "xu": xu_roofline(B, 197, cfg.inner_dim, cfg.state_dim, scan_ms, clk.summary())},
             "cpu_baseline": cpu,
             "ops": ops,
             "gpu_launches": 3 * cfg.depth * args.steps,  # rms_norm + conv1d+SiLU + fused scan per block
