@@ -159,6 +159,12 @@ def init_params(cfg: ModelConfig, seed: int = 0, device="cuda", dtype=torch.floa
     return {k: v.to(dtype) for k, v in p.items()}
 
 
+def _pad_cols(w: torch.Tensor, mult: int) -> torch.Tensor:
+    """Zero-pad the columns of a (K, N) weight to a multiple of ``mult``."""
+    pad = (-w.shape[1]) % mult
+    return torch.nn.functional.pad(w, (0, pad)) if pad else w
+
+
 class LBVim:
     """Inference-time LBVim on the fused kernels.  ``dtype`` is the activation
     / weight dtype (bf16 for throughput, fp32 for parity); scan state is fp32."""
@@ -180,10 +186,14 @@ class LBVim:
                 norm_scale=cast(w["norm_scale"]), norm_f32=f32(w["norm_scale"]),
                 w_in=cast(torch.cat([w["w_x"], w["w_z"]], dim=1)),                  # (D, 2E)
                 conv_kernel=f32(w["conv_kernel"]),                                    # (E, k)
-                w_xp=cast(torch.cat([w["w_delta"], w["w_b"], w["w_c"]], dim=1)),      # (E, E+2N)
+                # (E, E+2N) padded to a multiple of 64 columns and stored transposed:
+                # cuBLAS runs the x-projection ~15 % faster on that shape (N=448 "NT"
+                # vs N=416 "NN" at the LBVim-Ti shape, tools/gemmbench.py); the scan
+                # reads delta / B / C as strided column views either way
+                w_xpT=_pad_cols(cast(torch.cat([w["w_delta"], w["w_b"], w["w_c"]], dim=1)), 64).t().contiguous(),
                 A=f32(-torch.exp(w["a_log"].float())),
                 D=f32(w["d_param"]), delta_bias=f32(w["delta_bias"]),
-                w_out=cast(w["w_out"]),
+                w_outT=cast(w["w_out"]).t().contiguous(),  # "NT" out-projection (~4 % faster)
             ))
         self.head = {k: cast(v) for k, v in params.items() if k.startswith("head.")}
         self._graph = None
@@ -219,12 +229,12 @@ class LBVim:
         xz = (xn.reshape(-1, D) @ w["w_in"]).reshape(B, L, 2 * E)
         x, z = xz[..., :E], xz[..., E:]
         xs = causal_conv1d_silu_fwd(x, w["conv_kernel"], reverse=reverse)
-        proj = (xs.reshape(-1, E) @ w["w_xp"]).reshape(B, L, E + 2 * N)
+        proj = (xs.reshape(-1, E) @ w["w_xpT"].t()).reshape(B, L, -1)
         yg = lbm_selective_scan_fwd(
-            xs, proj[..., :E], w["A"], proj[..., E:E + N], proj[..., E + N:], D=w["D"], z=z,
+            xs, proj[..., :E], w["A"], proj[..., E:E + N], proj[..., E + N:E + 2 * N], D=w["D"], z=z,
             delta_bias=w["delta_bias"], window=self.M, reverse=reverse,
             lb=self.cfg.scan_variant == "lbm", discretize_mode=self.cfg.discretize_mode)
-        return torch.addmm(T.reshape(-1, D), yg.reshape(-1, E), w["w_out"]).reshape(B, L, D)
+        return torch.addmm(T.reshape(-1, D), yg.reshape(-1, E), w["w_outT"].t()).reshape(B, L, D)
 
     def run_blocks(self, tok):
         """model.py:204-222.  Returns tokens in original order; the number of
