@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(kConvTileE) conv_fwd_smem_kernel(ConvParams p)
 // (K-1 history in registers) into an output tile, and the tile leaves as
 // coalesced 16-byte stores -- every HBM access is a whole 16-byte piece.
 // Flip-on-load: logical row l is physical L-1-l for both the input and output.
+#ifndef LBS_CONV_PAIR
+#define LBS_CONV_PAIR 1  // two channels per thread for whole 128-channel tiles
+#endif
 #ifndef LBS_CONV_TT
 #define LBS_CONV_TT 32
 #endif
@@ -327,6 +330,91 @@ __global__ void __launch_bounds__(kConvTE) conv_fwd_tile_kernel(ConvParams p) {
     const int l = l0 + j;
     *reinterpret_cast<uint4*>(ob + (long long)(rev ? L - 1 - l : l) * p.so1 + pc * V) =
         *reinterpret_cast<const uint4*>(&yout[j][pc * V]);
+  }
+}
+
+// Two-channel variant of the tile kernel (default for whole 128-channel tiles):
+// 64 threads per (b, 32-step, 128-channel) tile, each thread sweeps a channel
+// PAIR -- one 4-byte (bf16) / 8-byte (fp32) shared-memory access, packed FFMA2
+// taps and one F2FP per two outputs -- and the staging index math is
+// compile-time (16-byte pieces per row = 128 / V).  The single-channel kernel
+// issued ~32 instructions per output (77 % issue-active, ncu) against ~17 here.
+template <typename T, int KW>
+__global__ void __launch_bounds__(kConvTE / 2) conv_fwd_tile2_kernel(ConvParams p) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int NT = kConvTE / 2;      // threads
+  constexpr int PPR = kConvTE / V;     // 16-byte pieces per row
+  constexpr int ROWS = kConvTT + KW - 1;
+  __shared__ __align__(16) T xin[ROWS][kConvTE];
+  __shared__ __align__(16) T yout[kConvTT][kConvTE];
+  const int e0 = blockIdx.x * kConvTE;
+  const int l0 = blockIdx.y * kConvTT;
+  const int b = blockIdx.z;
+  const int L = p.L;
+  const int TT = min(kConvTT, L - l0);
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
+#pragma unroll
+  for (int i0 = 0; i0 < ROWS * PPR; i0 += NT) {
+    const int i = i0 + threadIdx.x;
+    const int r = i / PPR, pc = i % PPR;
+    const int l = l0 - (KW - 1) + r;
+    if (i < ROWS * PPR) {
+      T* dst = &xin[r][pc * V];
+      if (l >= 0 && l < L) cp_async16_conv(dst, xb + (long long)(rev ? L - 1 - l : l) * p.x.s1 + pc * V);
+      else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  {
+    const int c = 2 * threadIdx.x;
+    const int e = e0 + c;
+    f2 w[KW];
+#pragma unroll
+    for (int q = 0; q < KW; ++q)
+      w[q] = q < p.K ? mk2(p.w[(long long)e * p.K + q], p.w[(long long)(e + 1) * p.K + q]) : mk2(0.f, 0.f);
+    const f2 bias = p.bias ? mk2(p.bias[e], p.bias[e + 1]) : mk2(0.f, 0.f);
+    auto ld2 = [&](int r) -> f2 {
+      if constexpr (sizeof(T) == 4) {
+        const float2 v = *reinterpret_cast<const float2*>(&xin[r][c]);
+        return mk2(v.x, v.y);
+      } else {
+        const unsigned u = *reinterpret_cast<const unsigned*>(&xin[r][c]);
+        return mk2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+      }
+    };
+    f2 hist[KW];  // hist[q] = x[l - q] for the two channels
+#pragma unroll
+    for (int q = 1; q < KW; ++q) hist[q] = ld2(KW - 1 - q);
+#pragma unroll 8
+    for (int j = 0; j < kConvTT; ++j) {
+      hist[0] = ld2(KW - 1 + j);
+      f2 acc = bias;
+#pragma unroll
+      for (int q = KW - 1; q >= 0; --q) acc = fma2(w[q], hist[q], acc);
+      if (act) acc = mk2(silu_f(acc.x), silu_f(acc.y));
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float2*>(&yout[j][c]) = make_float2(acc.x, acc.y);
+      } else {
+        *reinterpret_cast<__nv_bfloat162*>(&yout[j][c]) = __floats2bfloat162_rn(acc.x, acc.y);
+      }
+#pragma unroll
+      for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
+    }
+  }
+  __syncthreads();
+  T* ob = static_cast<T*>(p.out) + (long long)b * p.so0 + e0;
+#pragma unroll
+  for (int i0 = 0; i0 < kConvTT * PPR; i0 += NT) {
+    const int i = i0 + threadIdx.x;
+    const int j = i / PPR, pc = i % PPR;
+    if (j < TT) {
+      const int l = l0 + j;
+      *reinterpret_cast<uint4*>(ob + (long long)(rev ? L - 1 - l : l) * p.so1 + pc * V) =
+          *reinterpret_cast<const uint4*>(&yout[j][pc * V]);
+    }
   }
 }
 
@@ -418,6 +506,14 @@ static bool conv_vec_ok(const ConvParams& p) {
 
 template <typename T>
 static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
+  if constexpr (std::is_same<T, float>::value || std::is_same<T, __nv_bfloat16>::value) {
+    if (conv_vec_ok<T>(p) && LBS_CONV_SMEM == 2 && LBS_CONV_PAIR && p.E % kConvTE == 0) {
+      dim3 grid(p.E / kConvTE, (p.L + kConvTT - 1) / kConvTT, p.Bt);
+      if (p.K <= 4) conv_fwd_tile2_kernel<T, 4><<<grid, kConvTE / 2, 0, st>>>(p);
+      else conv_fwd_tile2_kernel<T, kMaxWidth><<<grid, kConvTE / 2, 0, st>>>(p);
+      return cudaGetLastError();
+    }
+  }
   if (conv_vec_ok<T>(p) && LBS_CONV_SMEM == 2) {
     dim3 grid((p.E + kConvTE - 1) / kConvTE, (p.L + kConvTT - 1) / kConvTT, p.Bt);
     if (p.K <= 4) conv_fwd_tile_kernel<T, 4><<<grid, kConvTE, 0, st>>>(p);
