@@ -74,6 +74,61 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const T* __restrict__ x, 
   }
 }
 
+// G lanes per row (G | 32, 32/G rows per warp), VPL 16-byte vectors per lane:
+// every lane busy and 32/G rows of loads in flight per warp (D = 192 bf16 is 24
+// vectors: 8 lanes x 3 instead of 24 of 32 lanes x 1).
+template <typename T, int G, int VPL>
+__global__ void __launch_bounds__(256) rms_norm_group_kernel(const T* __restrict__ x, const float* __restrict__ scale,
+                                                             T* __restrict__ out, long long rows, int D, float eps,
+                                                             long long sx, long long so) {
+  constexpr int EPV = 16 / sizeof(T);
+  const int lane = threadIdx.x % 32;
+  const int sub = lane % G;
+  const long long row = ((long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32) * (32 / G) + lane / G;
+  const bool ok = row < rows;
+  uint4 raw[VPL];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c0 = (sub + G * k) * EPV;
+    raw[k] = (ok && c0 < D) ? *reinterpret_cast<const uint4*>(x + row * sx + c0) : make_uint4(0, 0, 0, 0);
+  }
+  float v[VPL][EPV];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const T* e = reinterpret_cast<const T*>(&raw[k]);
+#pragma unroll
+    for (int i = 0; i < EPV; ++i) {
+      v[k][i] = to_f(e[i]);
+      ss = fmaf(v[k][i], v[k][i], ss);
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float inv = rsqrtf(ss / (float)D + eps);
+  if (!ok) return;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c0 = (sub + G * k) * EPV;
+    if (c0 < D) {
+      uint4 o4;
+      T* e = reinterpret_cast<T*>(&o4);
+#pragma unroll
+      for (int i = 0; i < EPV; i += 4) {
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>(scale + c0 + i));
+        const float sc[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float y = v[k][i + u] * inv * sc[u];
+          if constexpr (sizeof(T) == 4) e[i + u] = y;
+          else e[i + u] = __float2bfloat16_rn(y);
+        }
+      }
+      *reinterpret_cast<uint4*>(out + row * so + c0) = o4;
+    }
+  }
+}
+
 // any D / alignment: one warp per row, scalar strided accesses
 template <typename T>
 __global__ void __launch_bounds__(256) rms_norm_scalar_kernel(const T* __restrict__ x, const float* __restrict__ scale,
@@ -110,6 +165,29 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
 #ifndef LBS_NORM_RPW
 #define LBS_NORM_RPW 1  // rows per warp (2, 4, 8 measured no better)
 #endif
+#ifndef LBS_NORM_GROUP
+#define LBS_NORM_GROUP 1
+#endif
+  if (LBS_NORM_GROUP) {
+    // smallest power-of-two lane group with <= 3 vectors per lane
+    const int nv = p.D / EPV;
+    int G = 1;
+    while (G < 32 && (nv + G - 1) / G > 3) G *= 2;
+    const int vpl = (nv + G - 1) / G;
+    if (vpl <= 3) {
+      const long long rows_per_block = 8LL * (32 / G);
+      dim3 gg((unsigned)((p.rows + rows_per_block - 1) / rows_per_block));
+#define LBS_NORM_G(GG)                                                                                     \
+  if (G == GG) {                                                                                           \
+    if (vpl == 1) rms_norm_group_kernel<T, GG, 1><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
+    else if (vpl == 2) rms_norm_group_kernel<T, GG, 2><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
+    else rms_norm_group_kernel<T, GG, 3><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
+    return cudaGetLastError();                                                                             \
+  }
+      LBS_NORM_G(1) LBS_NORM_G(2) LBS_NORM_G(4) LBS_NORM_G(8) LBS_NORM_G(16) LBS_NORM_G(32)
+#undef LBS_NORM_G
+    }
+  }
   constexpr int RPW = LBS_NORM_RPW;
   dim3 gridv((unsigned)((p.rows + 8 * RPW - 1) / (8 * RPW)));
   if (vpl <= 1) rms_norm_kernel<T, 1, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
