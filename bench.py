@@ -267,7 +267,20 @@ def measure_ops(peak, iters=10):
     res["cfg5_model"] = {"what": "configs[4] MambaMIL-style bag forward (fc 1024->512, RMSNorm, in-proj, conv, "
                                  "x_proj, LB scan E=512 N=16 M=16, mean pool, head), L=100k, bf16, 1 GPU",
                          "ms_per_bag": ms, "bags_per_s": 1e3 / ms}
-    del bag, X, flush
+    del bag, X
+    torch.cuda.empty_cache()
+    # configs[2] as a workload: one LBVim-S training step (fwd + bwd through the fused
+    # scan / conv kernels, cuBLAS fp32 GEMMs, AdamW), batch 128, fp32
+    from paper_2506_15976_b200 import model as M
+    tcfg = M.lbvim_small()
+    tr = M.LBVimTrainer(tcfg, M.init_params(tcfg, seed=0, device="cuda"), lr=1e-4)
+    ti = torch.randn(128, 224, 224, 3, generator=g, device="cuda")
+    tl = torch.randint(0, tcfg.num_classes, (128,), generator=g, device="cuda")
+    ms = time_fn(lambda: tr.step(ti, tl), 3, flush)
+    res["cfg3_train"] = {"what": "configs[2] LBVim-S training step (fwd+bwd+AdamW), batch 128, fp32, 24 layers, "
+                                 "fused scan fwd/bwd + conv fwd/bwd, cuBLAS fp32 GEMMs",
+                         "ms_per_step": ms, "images_per_s": 128 / ms * 1e3}
+    del tr, ti, tl, flush
     torch.cuda.empty_cache()
     return res
 
