@@ -485,15 +485,154 @@ __global__ void __launch_bounds__(kConvThreads) conv_bwd_kernel(ConvParams p) {
   part[K] = db;
 }
 
-// deterministic reduction of the (B * n_chunks) partials -> dweight, dbias (+=)
-__global__ void conv_reduce_kernel(const float* part, int n_part, int E, int K, float* dw, float* db) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= E * (K + 1)) return;
+// Tile-staged backward (16-byte aligned rows): a 64-thread CTA owns (b, 32-step
+// chunk, 64 channels).  x rows [l0-(K-1), l0+32+K-1) and dout rows [l0, l0+32+K-1)
+// arrive by cp.async 16-byte pieces; each thread recomputes g = dout * silu'(xc)
+// for its channel from shared memory and slides the K-step window exactly as
+// conv_bwd_kernel does (same operation order: identical dx and partials); dx
+// leaves through a shared-memory tile as 16-byte stores.  The scalar kernel
+// re-read x K+1 times per step through L1 (0.2 of HBM at the LBVim-S shape).
+constexpr int kConvBE = 64;
+template <typename T, int KW>
+__global__ void __launch_bounds__(kConvBE) conv_bwd_tile_kernel(ConvParams p) {
+  constexpr int V = 16 / sizeof(T);
+  constexpr int TT = kConvChunk;
+  constexpr int XR = TT + 2 * KW;  // x rows: l0-(KW-1) .. l0+TT+KW (the register window reads 2 past)
+  constexpr int GR = TT + KW - 1;        // dout rows: l0 .. l0+TT+KW-2
+  __shared__ __align__(16) T xs[XR][kConvBE];
+  __shared__ __align__(16) T gs[GR][kConvBE];
+  __shared__ __align__(16) T dxo[TT][kConvBE];
+  const int e0 = blockIdx.x * kConvBE;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  const int l0 = chunk * TT;
+  const int L = p.L;
+  constexpr int K = KW;  // launched only for K == KW (exact window: no predicated copies)
+  const int EC = min(kConvBE, p.E - e0);
+  const int ppr = EC / V;
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
+  const T* gb = static_cast<const T*>(p.dout.p) + (long long)b * p.dout.s0 + e0;
+  for (int i = threadIdx.x; i < (XR + GR) * ppr; i += kConvBE) {
+    const int r = i / ppr, pc = i - r * ppr;
+    const bool isx = r < XR;
+    const int l = isx ? l0 - (KW - 1) + r : l0 + (r - XR);
+    T* dst = isx ? &xs[r][pc * V] : &gs[r - XR][pc * V];
+    if (l >= 0 && l < L) {
+      const long long ph = rev ? L - 1 - l : l;
+      cp_async16_conv(dst, isx ? xb + ph * p.x.s1 + pc * V : gb + ph * p.dout.s1 + pc * V);
+    } else {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const int c = threadIdx.x;
+  const int l1 = min(L, l0 + TT);
+  if (c < EC) {
+    const int e = e0 + c;
+    float w[KW];
+#pragma unroll
+    for (int q = 0; q < KW; ++q) w[q] = q < K ? p.w[(long long)e * K + q] : 0.f;
+    const float bias = p.bias ? p.bias[e] : 0.f;
+    auto X = [&](int l) -> float { return to_f(xs[l - l0 + (KW - 1)][c]); };  // zero-padded rows
+    // x in a register window: xw[i] = x[l - (KW-1) + i], i < 2 KW (one new row per step)
+    float xw[2 * KW];
+#pragma unroll
+    for (int i = 0; i < 2 * KW; ++i) xw[i] = X(l0 - (KW - 1) + i);
+    // g = dout * silu'(xc) at l + off, from the window (off in [0, KW])
+    auto Gw = [&](int l, int off) -> float {
+      if (l + off >= L) return 0.f;
+      float gv = to_f(gs[l + off - l0][c]);
+      if (act) {
+        float xc = bias;
+#pragma unroll
+        for (int q = 0; q < KW; ++q)
+          if (q < K) xc = fmaf(w[q], xw[KW - 1 + off - q], xc);
+        const float sg = sigmoid_f(xc);
+        gv *= sg * (1.f + xc * (1.f - sg));
+      }
+      return gv;
+    };
+    float dw[KW];
+#pragma unroll
+    for (int q = 0; q < KW; ++q) dw[q] = 0.f;
+    float db = 0.f;
+    float fut[KW];  // fut[q] = g[l + q]
+#pragma unroll
+    for (int q = 0; q < KW; ++q) fut[q] = (q < K) ? Gw(l0, q) : 0.f;
+#pragma unroll 4
+    for (int l = l0; l < l1; ++l) {
+      float acc = 0.f;
+#pragma unroll
+      for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], fut[q], acc);
+      dxo[l - l0][c] = from_f<T>(acc);
+      const float g0 = fut[0];
+      db += g0;
+#pragma unroll
+      for (int q = 0; q < KW; ++q)
+        if (q < K) dw[q] = fmaf(g0, xw[KW - 1 - q], dw[q]);
+#pragma unroll
+      for (int q = 0; q < KW - 1; ++q) fut[q] = fut[q + 1];
+      fut[KW - 1] = 0.f;
+      fut[K - 1] = Gw(l, K);
+      // slide the x window one step
+#pragma unroll
+      for (int i = 0; i < 2 * KW - 1; ++i) xw[i] = xw[i + 1];
+      xw[2 * KW - 1] = X(l + KW + 1);
+    }
+    float* part = p.part + (((long long)b * p.n_chunks + chunk) * p.E + e) * (K + 1);
+    for (int q = 0; q < K; ++q) part[q] = dw[q];
+    part[K] = db;
+  }
+  __syncthreads();
+  T* ob = static_cast<T*>(p.dx) + (long long)b * p.sd0 + e0;
+  for (int i = threadIdx.x; i < (l1 - l0) * ppr; i += kConvBE) {
+    const int j = i / ppr, pc = i - j * ppr;
+    const int l = l0 + j;
+    *reinterpret_cast<uint4*>(ob + (long long)(rev ? L - 1 - l : l) * p.sd1 + pc * V) =
+        *reinterpret_cast<const uint4*>(&dxo[j][pc * V]);
+  }
+}
+
+// deterministic reduction of the (B * n_chunks) partials -> dweight, dbias (+=).
+// A 1024-thread block owns 32 consecutive (e, q) outputs: 32 slices of threads
+// each sum every 32nd partial (fp64, fixed order, 4 loads in flight), then the
+// 32 slice sums are added in fixed order.  (One thread per output walking all
+// partials serially was a ~900-deep load chain: 134 us at the LBVim-S shape.)
+constexpr int kRedSlices = 32;
+__global__ void __launch_bounds__(32 * kRedSlices) conv_reduce_kernel(const float* part, int n_part, int E, int K,
+                                                                       float* dw, float* db) {
+  __shared__ double acc[kRedSlices][33];
+  const int lane = threadIdx.x % 32, slice = threadIdx.x / 32;
+  const int idx = blockIdx.x * 32 + lane;
+  const int n = E * (K + 1);
   double s = 0.0;
-  for (int i = 0; i < n_part; ++i) s += part[(long long)i * E * (K + 1) + idx];
-  const int e = idx / (K + 1), q = idx - e * (K + 1);
-  if (q < K) dw[(long long)e * K + q] += (float)s;
-  else if (db) db[e] += (float)s;
+  if (idx < n) {
+    const long long stride = (long long)n;
+    int i = slice;
+    for (; i + 3 * kRedSlices < n_part; i += 4 * kRedSlices) {
+      const float a0 = part[(long long)i * stride + idx];
+      const float a1 = part[(long long)(i + kRedSlices) * stride + idx];
+      const float a2 = part[(long long)(i + 2 * kRedSlices) * stride + idx];
+      const float a3 = part[(long long)(i + 3 * kRedSlices) * stride + idx];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; i < n_part; i += kRedSlices) s += part[(long long)i * stride + idx];
+  }
+  acc[slice][lane] = s;
+  __syncthreads();
+  if (slice == 0 && idx < n) {
+    double t = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < kRedSlices; ++k) t += acc[k][lane];
+    const int e = idx / (K + 1), q = idx - e * (K + 1);
+    if (q < K) dw[(long long)e * K + q] += (float)t;
+    else if (db) db[e] += (float)t;
+  }
 }
 
 template <typename T>
@@ -502,6 +641,18 @@ static bool conv_vec_ok(const ConvParams& p) {
   auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
   return p.E % V == 0 && p.x.s2 == 1 && p.so2 == 1 && al(p.x.p) && al(p.out) && p.x.s0 % V == 0 &&
          p.x.s1 % V == 0 && p.so0 % V == 0 && p.so1 % V == 0;
+}
+
+#ifndef LBS_CONV_BWD_TILE
+#define LBS_CONV_BWD_TILE 1
+#endif
+template <typename T>
+static bool conv_bwd_vec_ok(const ConvParams& p) {
+  constexpr int V = 16 / sizeof(T);
+  auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+  return p.E % V == 0 && p.x.s2 == 1 && p.dout.s2 == 1 && p.sd2 == 1 && al(p.x.p) && al(p.dout.p) && al(p.dx) &&
+         p.x.s0 % V == 0 && p.x.s1 % V == 0 && p.dout.s0 % V == 0 && p.dout.s1 % V == 0 && p.sd0 % V == 0 &&
+         p.sd1 % V == 0;
 }
 
 template <typename T>
@@ -545,10 +696,16 @@ static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
 template <typename T>
 static cudaError_t conv_bwd_t(const ConvParams& p, float* dw, float* db, cudaStream_t st) {
   dim3 grid((p.E + kConvThreads - 1) / kConvThreads, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
-  if (p.K <= 4) conv_bwd_kernel<T, 4><<<grid, kConvThreads, 0, st>>>(p);
-  else conv_bwd_kernel<T, kMaxWidth><<<grid, kConvThreads, 0, st>>>(p);
+  if (conv_bwd_vec_ok<T>(p) && LBS_CONV_BWD_TILE && p.K == 4) {
+    dim3 gt((p.E + kConvBE - 1) / kConvBE, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
+    conv_bwd_tile_kernel<T, 4><<<gt, kConvBE, 0, st>>>(p);
+  } else if (p.K <= 4) {
+    conv_bwd_kernel<T, 4><<<grid, kConvThreads, 0, st>>>(p);
+  } else {
+    conv_bwd_kernel<T, kMaxWidth><<<grid, kConvThreads, 0, st>>>(p);
+  }
   const int n = p.E * (p.K + 1);
-  conv_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(p.part, p.Bt * p.n_chunks, p.E, p.K, dw, db);
+  conv_reduce_kernel<<<(n + 31) / 32, 32 * kRedSlices, 0, st>>>(p.part, p.Bt * p.n_chunks, p.E, p.K, dw, db);
   return cudaGetLastError();
 }
 

@@ -40,3 +40,18 @@ for name, (B, L, D) in {"cfg2": (256, 197, 192), "cfg4": (32, 4097, 384)}.items(
     nb = 2 * 2 * B * L * D
     print(json.dumps(dict(cfg=name, kernel="rms_norm", ms=round(ms, 4), gbs=round(nb / ms / 1e6, 1),
                           frac=round(nb / ms / 1e6 / peak, 3))), flush=True)
+
+# backward (training shapes): reads x, dout, writes dx (+ weight-grad partials)
+from paper_2506_15976_b200.conv import causal_conv1d_silu_bwd  # noqa: E402
+for name, (B, L, E, dt) in {"cfg3_bwd_f32": (128, 197, 768, torch.float32),
+                            "cfg2_bwd_bf16": (256, 197, 384, torch.bfloat16)}.items():
+    x = torch.randn(B, L, E, device="cuda").to(dt)
+    g = torch.randn(B, L, E, device="cuda").to(dt)
+    w = torch.randn(E, 4, device="cuda")
+    bias = torch.randn(E, device="cuda")
+    s = torch.tensor([], dtype=dt).element_size()
+    for rev in (False, True):
+        ms = time_fn(lambda: causal_conv1d_silu_bwd(x, w, bias, g, reverse=rev), a.iters, flush)
+        nb = 3 * s * B * L * E
+        print(json.dumps(dict(cfg=name, kernel="conv_bwd", reverse=rev, ms=round(ms, 4),
+                              gbs=round(nb / ms / 1e6, 1), frac=round(nb / ms / 1e6 / peak, 3))), flush=True)
