@@ -258,6 +258,37 @@ def test_conv_fwd_vectorised(dtype, K, reverse):
     assert O.max_rel_err(got, ref) <= (TOL_F32 if dtype == torch.float32 else 1e-2)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("E", [256, 96])
+@pytest.mark.parametrize("reverse", [False, True])
+def test_conv_tile_kernels_fwd_bwd(dtype, E, reverse):
+    """The 128-channel pair forward kernel (E % 128 == 0) / single-channel tile kernel
+    (E = 96), and the tile-staged backward (K = 4, 64-channel tiles, partial tile at
+    E = 96), on column views of a wider projection, L with a ragged 32-step chunk,
+    with a bias; against the oracle on the same (rounded) inputs."""
+    from paper_2506_15976_b200.conv import causal_conv1d_silu_bwd, causal_conv1d_silu_fwd
+    rng = O.seeded_rng(E + 3 * reverse)
+    Bt, L, K = 2, 101, 4
+    xz = dev(rng.standard_normal((Bt, L, 2 * E)), dtype)
+    x = xz[..., :E]
+    gz = dev(rng.standard_normal((Bt, L, 2 * E)), dtype)
+    g = gz[..., E:]
+    w = rng.standard_normal((E, K)) * 0.5
+    bias = rng.standard_normal(E) * 0.1
+    xq, gq = x.double().cpu().numpy(), g.double().cpu().numpy()
+    flip = (lambda a: a[:, ::-1]) if reverse else (lambda a: a)
+    xc = O.causal_conv1d(flip(xq), w) + bias
+    tol = TOL_F32 if dtype == torch.float32 else 1e-2
+    got = causal_conv1d_silu_fwd(x, dev(w), dev(bias), reverse=reverse).double().cpu().numpy()
+    assert O.max_rel_err(got, flip(O.silu(xc))) <= tol
+    gpre = flip(gq) * O.silu_grad(xc)
+    gx_ref, gw_ref = O.causal_conv1d_grad(flip(xq), w, gpre)
+    dx, dw, db = causal_conv1d_silu_bwd(x, dev(w), dev(bias), g, reverse=reverse)
+    assert O.max_rel_err(dx.double().cpu().numpy(), flip(gx_ref)) <= tol
+    assert O.max_rel_err(dw.cpu().numpy(), gw_ref) <= (1e-4 if dtype == torch.float32 else 1e-2)
+    assert O.max_rel_err(db.cpu().numpy(), gpre.sum((0, 1))) <= (1e-4 if dtype == torch.float32 else 1e-2)
+
+
 def test_conv_golden():
     from paper_2506_15976_b200.conv import causal_conv1d_silu_bwd, causal_conv1d_silu_fwd
     g = np.load(os.path.join(GOLD, "conv.npz"))
