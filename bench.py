@@ -280,6 +280,14 @@ def measure_ops(peak, iters=10):
     res["cfg3_train"] = {"what": "configs[2] LBVim-S training step (fwd+bwd+AdamW), batch 128, fp32, 24 layers, "
                                  "fused scan fwd/bwd + conv fwd/bwd, cuBLAS fp32 GEMMs",
                          "ms_per_step": ms, "images_per_s": 128 / ms * 1e3}
+    del tr
+    torch.cuda.empty_cache()
+    tr = M.LBVimTrainer(tcfg, M.init_params(tcfg, seed=0, device="cuda"), lr=1e-4, amp=True)
+    ms = time_fn(lambda: tr.step(ti, tl), 3, flush)
+    res["cfg3_train_bf16"] = {"what": "configs[2] LBVim-S training step, bf16 autocast projections (tensor cores), "
+                                      "bf16-I/O fused scan / conv kernels with fp32 state, fp32 master weights + AdamW, "
+                                      "batch 128",
+                              "ms_per_step": ms, "images_per_s": 128 / ms * 1e3}
     del tr, ti, tl, flush
     torch.cuda.empty_cache()
     return res

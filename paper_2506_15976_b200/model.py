@@ -333,8 +333,13 @@ class LBVimTrainer:
     Mirrors autodiff.train_step (autodiff.py:293-314) for the GAP / class-token
     heads; blocks alternate direction by flip-on-load as in ``LBVim``."""
 
-    def __init__(self, cfg: ModelConfig, params: dict, lr: float = 1e-3, weight_decay: float = 0.05):
+    def __init__(self, cfg: ModelConfig, params: dict, lr: float = 1e-3, weight_decay: float = 0.05,
+                 amp: bool = False):
+        """``amp=True``: bf16 autocast for the projections (tensor cores), so the fused
+        scan / conv kernels run their bf16-I/O variants (fp32 state, fp32 master
+        weights and optimizer); default fp32 throughout, like the reference."""
         self.cfg = cfg
+        self.amp = amp
         self.M = cfg.resolved_tile_len
         self.params = {k: v.detach().clone().float().requires_grad_(True) for k, v in params.items()}
         self.opt = torch.optim.AdamW(self.params.values(), lr=lr, weight_decay=weight_decay)
@@ -370,7 +375,9 @@ class LBVimTrainer:
     def step(self, images, labels):
         """One optimisation step; returns the loss tensor (no host sync)."""
         self.opt.zero_grad(set_to_none=True)
-        loss = F.cross_entropy(self.forward(images), labels)
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=self.amp):
+            logits = self.forward(images)
+        loss = F.cross_entropy(logits.float(), labels)
         loss.backward()
         self.opt.step()
         return loss.detach()
