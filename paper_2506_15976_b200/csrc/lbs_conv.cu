@@ -253,6 +253,9 @@ __global__ void __launch_bounds__(kConvTileE) conv_fwd_smem_kernel(ConvParams p)
 // (K-1 history in registers) into an output tile, and the tile leaves as
 // coalesced 16-byte stores -- every HBM access is a whole 16-byte piece.
 // Flip-on-load: logical row l is physical L-1-l for both the input and output.
+#ifndef LBS_CONV_INPLACE
+#define LBS_CONV_INPLACE 1
+#endif
 #ifndef LBS_CONV_PAIR
 #define LBS_CONV_PAIR 1  // two channels per thread for whole 128-channel tiles
 #endif
@@ -346,7 +349,15 @@ __global__ void __launch_bounds__(kConvTE / 2) conv_fwd_tile2_kernel(ConvParams 
   constexpr int PPR = kConvTE / V;     // 16-byte pieces per row
   constexpr int ROWS = kConvTT + KW - 1;
   __shared__ __align__(16) T xin[ROWS][kConvTE];
+#if LBS_CONV_INPLACE
+  // output row j overwrites input row j: this thread's columns of row j were
+  // last read KW-1 steps earlier (the history lives in registers), and the
+  // vector store phase runs after the barrier -- half the shared memory, twice
+  // the resident CTAs
+  T (*yout)[kConvTE] = xin;
+#else
   __shared__ __align__(16) T yout[kConvTT][kConvTE];
+#endif
   const int e0 = blockIdx.x * kConvTE;
   const int l0 = blockIdx.y * kConvTT;
   const int b = blockIdx.z;
@@ -498,10 +509,16 @@ __global__ void __launch_bounds__(kConvBE) conv_bwd_tile_kernel(ConvParams p) {
   constexpr int V = 16 / sizeof(T);
   constexpr int TT = kConvChunk;
   constexpr int XR = TT + 2 * KW;  // x rows: l0-(KW-1) .. l0+TT+KW (the register window reads 2 past)
-  constexpr int GR = TT + KW - 1;        // dout rows: l0 .. l0+TT+KW-2
+  constexpr int GR = TT + KW;            // dout rows: l0 .. l0+TT+KW-1 (the window's last, unused, lookahead reads row TT+K-1)
   __shared__ __align__(16) T xs[XR][kConvBE];
   __shared__ __align__(16) T gs[GR][kConvBE];
+#if LBS_CONV_INPLACE
+  // dx row j overwrites dout row j: this thread last read its column of that row
+  // K steps earlier (the g window lives in registers)
+  T (*dxo)[kConvBE] = gs;
+#else
   __shared__ __align__(16) T dxo[TT][kConvBE];
+#endif
   const int e0 = blockIdx.x * kConvBE;
   const int chunk = blockIdx.y, b = blockIdx.z;
   const int l0 = chunk * TT;
