@@ -69,7 +69,7 @@ struct BwdSmem {
   static constexpr size_t off_da = off_mu + pq_bytes;
   static constexpr size_t off_red = off_da + pq_bytes;
   static constexpr size_t off_raw = off_red + red_bytes;
-  static constexpr size_t tr_bytes = 4ull * (KT * 4) * 33 * sizeof(float);  // per-warp transpose [v][lane]
+  static constexpr size_t tr_bytes = 4ull * 32 * (KT * 4 + 4) * sizeof(float);  // per-warp transpose [lane][v]
   static constexpr size_t off_tr = off_raw + raw_bytes;
   // sigmoid(delta_pre) and sigmoid(z) of the chunk's steps, kept from the
   // prologue (which already has e^x / computes silu(z)) for the epilogue
@@ -310,11 +310,10 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
       }
 #if LBS_BWD_RED_SMEM
       // park the 4 values of step j in this warp's transpose buffer [v][lane]
-      float* tw = tr + (size_t)warp * (KT * 4) * 33;
-      tw[(j * 4 + 0) * 33 + lane] = dBv.x;
-      tw[(j * 4 + 1) * 33 + lane] = dBv.y;
-      tw[(j * 4 + 2) * 33 + lane] = dCv.x;
-      tw[(j * 4 + 3) * 33 + lane] = dCv.y;
+      // this lane's row [lane][v] of the warp's transpose buffer, row stride KT*4+4
+      // (= 4 mod 32: the 16-byte stores of a quarter-warp hit distinct banks)
+      float* tw = tr + (size_t)warp * 32 * (KT * 4 + 4);
+      *reinterpret_cast<float4*>(&tw[lane * (KT * 4 + 4) + j * 4]) = make_float4(dBv.x, dBv.y, dCv.x, dCv.y);
       (void)rv;
 #else
       const int o = (j & 3) * 4;
@@ -336,17 +335,17 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
     // warp sum of each of the KT*4 values: lane l owns values l, l+32, ...
     __syncwarp();
     {
-      const float* tw = tr + (size_t)warp * (KT * 4) * 33;
+      const float* tw = tr + (size_t)warp * 32 * (KT * 4 + 4);
 #pragma unroll
       for (int v0 = 0; v0 < KT * 4; v0 += 32) {
         const int vv = v0 + lane;
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
         for (int k = 0; k < 32; k += 4) {
-          s0 += tw[vv * 33 + k];
-          s1 += tw[vv * 33 + k + 1];
-          s2 += tw[vv * 33 + k + 2];
-          s3 += tw[vv * 33 + k + 3];
+          s0 += tw[k * (KT * 4 + 4) + vv];
+          s1 += tw[(k + 1) * (KT * 4 + 4) + vv];
+          s2 += tw[(k + 2) * (KT * 4 + 4) + vv];
+          s3 += tw[(k + 3) * (KT * 4 + 4) + vv];
         }
         const int jj = vv >> 2, kind = vv & 3;
         red[((warp * KT + jj) * 2 + (kind >> 1)) * NS + 2 * q + (kind & 1)] = (s0 + s1) + (s2 + s3);
