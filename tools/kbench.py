@@ -79,6 +79,17 @@ def time_fn(fn, iters, flush):
     return ts[len(ts) // 2]
 
 
+def gpu_warmup(seconds=0.5):
+    """Spin the GPU so its clocks have ramped before the first timed config."""
+    import time
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        for _ in range(20):
+            a = (a @ a).clamp_(-1, 1)
+        torch.cuda.synchronize()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
@@ -87,6 +98,7 @@ def main():
     a = ap.parse_args()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     peak = peak_gbs()
+    gpu_warmup()
     names = [n for n in CFGS if not a.only or n in a.only.split(",")]
     for name in names:
         Bt, L, E, N, M, io, bc = CFGS[name]

@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2506_15976_b200 import model as M  # noqa: E402
 
 cfg = M.lbvim_small()
-tr = M.LBVimTrainer(cfg, M.init_params(cfg, seed=0, device="cuda"), lr=1e-4)
+tr = M.LBVimTrainer(cfg, M.init_params(cfg, seed=0, device="cuda"), lr=1e-4, amp=bool(int(os.environ.get("AMP", 0))))
 x = torch.randn(int(os.environ.get("BATCH", 128)), 224, 224, 3, device="cuda")
 y = torch.randint(0, cfg.num_classes, (x.shape[0],), device="cuda")
 for _ in range(2):
