@@ -26,6 +26,7 @@ CFGS = {
     "cfg5": (1, 100000, 512, 16, 16, torch.float32, torch.float32),
     "cfg5s": (1, 100000, 64, 16, 16, torch.float32, torch.float32),
     "cfg3s": (16, 197, 768, 16, 8, torch.float32, torch.float32),  # configs[2] per-GPU shard at 8 GPUs
+    "cfg3b": (128, 197, 768, 16, 8, torch.bfloat16, torch.bfloat16),  # configs[2] shape, bf16 I/O (amp training)
 }
 
 
