@@ -218,9 +218,12 @@ def measure_ops(peak, iters=10):
              "cfg3": "configs[2] LBVim-S scan fp32 B=128 E=768 fwd+bwd", "cfg4": "configs[3] LBVim-S 1024^2 layer scan bf16 "
              "B=32 L=4096 E=768", "cfg5": "configs[4] MIL bag fp32 B=1 L=100k E=512 (1 GPU)",
              "cfg5s": "configs[4] one 8-way channel shard (E=64)",
-             "cfg3s": "configs[2] per-GPU batch shard at 8 GPUs (B=16) fwd+bwd"}
+             "cfg3s": "configs[2] per-GPU batch shard at 8 GPUs (B=16) fwd+bwd",
+             "cfg3b": "configs[2] shape with bf16 I/O (the amp training path) fwd+bwd"}
     res = {}
     for name, (Bt, L, E, N, M, io, bc) in CFGS.items():
+        if name not in names:
+            continue
         x = make(Bt, L, E, N, io, bc)
         out = torch.empty(Bt, L, E, device="cuda", dtype=io)
         s_io = torch.tensor([], dtype=io).element_size()
@@ -234,7 +237,7 @@ def measure_ops(peak, iters=10):
              "global_bidir_ms": bi_ms, "lb_over_bidir": (lb_ms / bi_ms) if bi_ms else None,
              "lb_over_fwd": lb_ms / fw_ms, "bytes": nb, "gbs": nb / lb_ms / 1e6, "frac": nb / lb_ms / 1e6 / peak,
              "lanes_per_s": Bt * L * E * N / lb_ms * 1e3}
-        if name in ("cfg3", "cfg3s"):
+        if name in ("cfg3", "cfg3s", "cfg3b"):
             dout = torch.randn(Bt, L, E, device="cuda").to(io)
             _, ck = lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True)
             nbb = bwd_alg_bytes(Bt, L, E, N, s_io, s_bc, s_io)
@@ -257,6 +260,34 @@ def measure_ops(peak, iters=10):
     res["cfg4_model"] = {"what": "configs[3] LBVim-S 1024^2 patch16 forward, batch 32, bf16, 24 layers, L=4097",
                          "ms_per_batch": ms, "images_per_s": 32 / ms * 1e3}
     del net, imgs, run
+    torch.cuda.empty_cache()
+    # the other hand-written kernels of the block at the LBVim shapes (HBM-bound):
+    # conv1d+SiLU fwd (2 s B L E bytes) and bwd (3 s B L E), RMSNorm (2 s B L D)
+    from paper_2506_15976_b200.conv import causal_conv1d_silu_bwd, causal_conv1d_silu_fwd
+    from paper_2506_15976_b200.norm import rms_norm
+    kern = {}
+    for tag, (Bk, Lk, Dk, dt) in {"lbvim_t": (256, 197, 192, torch.bfloat16),
+                                  "lbvim_s_1024": (32, 4097, 384, torch.bfloat16),
+                                  "lbvim_s_train_f32": (128, 197, 384, torch.float32)}.items():
+        Ek = 2 * Dk
+        sz = torch.tensor([], dtype=dt).element_size()
+        xz = torch.randn(Bk, Lk, 2 * Ek, generator=g, device="cuda").to(dt)
+        wk = torch.randn(Ek, 4, generator=g, device="cuda")
+        ok = torch.empty(Bk, Lk, Ek, device="cuda", dtype=dt)
+        ms_f = time_fn(lambda: causal_conv1d_silu_fwd(xz[..., :Ek], wk, out=ok), iters, flush)
+        gk = torch.randn(Bk, Lk, Ek, generator=g, device="cuda").to(dt)
+        ms_b = time_fn(lambda: causal_conv1d_silu_bwd(xz[..., :Ek], wk, None, gk), iters, flush)
+        tk = torch.randn(Bk, Lk, Dk, generator=g, device="cuda").to(dt)
+        sk = torch.randn(Dk, generator=g, device="cuda")
+        on = torch.empty_like(tk)
+        ms_n = time_fn(lambda: rms_norm(tk, sk, out=on), iters, flush)
+        nb_c, nb_n = 2 * sz * Bk * Lk * Ek, 2 * sz * Bk * Lk * Dk
+        kern[tag] = {"shape": [Bk, Lk, Ek], "dtype": str(dt).replace("torch.", ""),
+                     "conv_fwd_ms": ms_f, "conv_fwd_frac": nb_c / ms_f / 1e6 / peak,
+                     "conv_bwd_ms": ms_b, "conv_bwd_frac": 1.5 * nb_c / ms_b / 1e6 / peak,
+                     "rms_norm_ms": ms_n, "rms_norm_frac": nb_n / ms_n / 1e6 / peak}
+        del xz, ok, gk, tk, on
+    res["block_kernels"] = kern
     torch.cuda.empty_cache()
     # configs[4] as a workload: one MambaMIL-style bag (mil.py) on one GPU, bf16
     from paper_2506_15976_b200.mil import MILBag, MILConfig, init_mil_params
