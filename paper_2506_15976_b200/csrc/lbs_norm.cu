@@ -82,50 +82,65 @@ __global__ void __launch_bounds__(256) rms_norm_group_kernel(const T* __restrict
                                                              T* __restrict__ out, long long rows, int D, float eps,
                                                              long long sx, long long so) {
   constexpr int EPV = 16 / sizeof(T);
+  constexpr int RPWG = 32 / G;  // rows per warp per pass
   const int lane = threadIdx.x % 32;
   const int sub = lane % G;
-  const long long row = ((long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32) * (32 / G) + lane / G;
-  const bool ok = row < rows;
-  uint4 raw[VPL];
+  // grid-stride over row groups (the launcher sizes the grid to one resident wave);
+  // the next group's loads are issued before this group is reduced and stored
+  const long long warp0 = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const long long wstride = (long long)gridDim.x * (blockDim.x / 32) * RPWG;
+  auto load = [&](long long row, uint4 (&raw)[VPL]) {
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const int c0 = (sub + G * k) * EPV;
-    raw[k] = (ok && c0 < D) ? *reinterpret_cast<const uint4*>(x + row * sx + c0) : make_uint4(0, 0, 0, 0);
-  }
-  float v[VPL][EPV];
-  float ss = 0.f;
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const T* e = reinterpret_cast<const T*>(&raw[k]);
-#pragma unroll
-    for (int i = 0; i < EPV; ++i) {
-      v[k][i] = to_f(e[i]);
-      ss = fmaf(v[k][i], v[k][i], ss);
+    for (int k = 0; k < VPL; ++k) {
+      const int c0 = (sub + G * k) * EPV;
+      raw[k] = (row < rows && c0 < D) ? *reinterpret_cast<const uint4*>(x + row * sx + c0) : make_uint4(0, 0, 0, 0);
     }
-  }
+  };
+  long long wrow = warp0 * RPWG;  // first row of this warp's group (warp-uniform)
+  uint4 raw[VPL];
+  load(wrow + lane / G, raw);
+  for (; wrow < rows; wrow += wstride) {
+    const long long row = wrow + lane / G;
+    uint4 nxt[VPL];
+    load(wrow + wstride + lane / G, nxt);
+    float v[VPL][EPV];
+    float ss = 0.f;
 #pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float inv = rsqrtf(ss / (float)D + eps);
-  if (!ok) return;
+    for (int k = 0; k < VPL; ++k) {
+      const T* e = reinterpret_cast<const T*>(&raw[k]);
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const int c0 = (sub + G * k) * EPV;
-    if (c0 < D) {
-      uint4 o4;
-      T* e = reinterpret_cast<T*>(&o4);
+      for (int i = 0; i < EPV; ++i) {
+        v[k][i] = to_f(e[i]);
+        ss = fmaf(v[k][i], v[k][i], ss);
+      }
+    }
 #pragma unroll
-      for (int i = 0; i < EPV; i += 4) {
-        const float4 s4 = __ldg(reinterpret_cast<const float4*>(scale + c0 + i));
-        const float sc[4] = {s4.x, s4.y, s4.z, s4.w};
+    for (int o = G / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float inv = rsqrtf(ss / (float)D + eps);
+    if (row < rows) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float y = v[k][i + u] * inv * sc[u];
-          if constexpr (sizeof(T) == 4) e[i + u] = y;
-          else e[i + u] = __float2bfloat16_rn(y);
+      for (int k = 0; k < VPL; ++k) {
+        const int c0 = (sub + G * k) * EPV;
+        if (c0 < D) {
+          uint4 o4;
+          T* e = reinterpret_cast<T*>(&o4);
+#pragma unroll
+          for (int i = 0; i < EPV; i += 4) {
+            const float4 s4 = __ldg(reinterpret_cast<const float4*>(scale + c0 + i));
+            const float sc[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float y = v[k][i + u] * inv * sc[u];
+              if constexpr (sizeof(T) == 4) e[i + u] = y;
+              else e[i + u] = __float2bfloat16_rn(y);
+            }
+          }
+          *reinterpret_cast<uint4*>(out + row * so + c0) = o4;
         }
       }
-      *reinterpret_cast<uint4*>(out + row * so + c0) = o4;
     }
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) raw[k] = nxt[k];
   }
 }
 
@@ -165,6 +180,9 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
 #ifndef LBS_NORM_RPW
 #define LBS_NORM_RPW 1  // rows per warp (2, 4, 8 measured no better)
 #endif
+#ifndef LBS_NORM_PERSIST
+#define LBS_NORM_PERSIST 1
+#endif
 #ifndef LBS_NORM_GROUP
 #define LBS_NORM_GROUP 1
 #endif
@@ -176,7 +194,15 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
     const int vpl = (nv + G - 1) / G;
     if (vpl <= 3) {
       const long long rows_per_block = 8LL * (32 / G);
-      dim3 gg((unsigned)((p.rows + rows_per_block - 1) / rows_per_block));
+      static const int n_sms = [] {
+        int d = 0, n = 148;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+        return n;
+      }();
+      long long nb = (p.rows + rows_per_block - 1) / rows_per_block;
+      if (LBS_NORM_PERSIST && nb > (long long)n_sms * 8) nb = (long long)n_sms * 8;  // one resident wave
+      dim3 gg((unsigned)nb);
 #define LBS_NORM_G(GG)                                                                                     \
   if (G == GG) {                                                                                           \
     if (vpl == 1) rms_norm_group_kernel<T, GG, 1><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
