@@ -206,20 +206,33 @@ class LBVim:
         if H != cfg.image_size or W != cfg.image_size or C != cfg.in_channels:
             raise ShapeError(f"image shape {tuple(images.shape[1:])} does not match config")
         p, g = cfg.patch_size, cfg.image_size // cfg.patch_size
+        # (a channels_last stride-p cuDNN convolution instead of this patchify copy measured
+        # 12x slower: cuDNN converted to NCHW and ran an SIMT kernel)
         x = images.to(self.dtype).reshape(B, g, p, g, p, C).permute(0, 1, 3, 2, 4, 5).reshape(B, g * g, p * p * C)
         tok = torch.addmm(self.patch_b, x.reshape(-1, x.shape[-1]), self.patch_w).reshape(B, g * g, -1)
         ct = cfg.class_token
-        if ct != "none":
-            cls = self.cls
-            D = tok.shape[-1]
-            if ct == "head":
-                tok = torch.cat([cls[0].expand(B, 1, D), tok], 1)
-            elif ct == "middle":
-                mid = tok.shape[1] // 2
-                tok = torch.cat([tok[:, :mid], cls[0].expand(B, 1, D), tok[:, mid:]], 1)
-            else:
-                tok = torch.cat([cls[0].expand(B, 1, D), tok, cls[1].expand(B, 1, D)], 1)
-        return (tok + self.pos).contiguous()
+        D = tok.shape[-1]
+        if ct == "none":
+            return (tok + self.pos).contiguous()
+        # class token(s) and the position add written straight into the token buffer
+        L = self.pos.shape[0]
+        out = torch.empty(B, L, D, dtype=tok.dtype, device=tok.device)
+        pos = self.pos  # (L, D)
+        if ct == "head":
+            spans = [(1, 0, g * g)]
+            cls_at = [(0, 0)]
+        elif ct == "middle":
+            mid = (g * g) // 2
+            spans = [(0, 0, mid), (mid + 1, mid, g * g)]
+            cls_at = [(mid, 0)]
+        else:
+            spans = [(1, 0, g * g)]
+            cls_at = [(0, 0), (L - 1, 1)]
+        for dst, lo, hi in spans:
+            torch.add(tok[:, lo:hi], pos[dst:dst + hi - lo], out=out[:, dst:dst + hi - lo])
+        for dst, k in cls_at:
+            torch.add(self.cls[k].expand(B, D), pos[dst], out=out[:, dst])
+        return out
 
     def block(self, T, w, reverse: bool):
         """block.py:158-190 with the output reversal replaced by direction."""
