@@ -208,7 +208,13 @@ class LBVim:
         p, g = cfg.patch_size, cfg.image_size // cfg.patch_size
         # (a channels_last stride-p cuDNN convolution instead of this patchify copy measured
         # 12x slower: cuDNN converted to NCHW and ran an SIMT kernel)
-        x = images.to(self.dtype).reshape(B, g, p, g, p, C).permute(0, 1, 3, 2, 4, 5).reshape(B, g * g, p * p * C)
+        xi = images.to(self.dtype).reshape(B * g, p, g, p * C)  # (b gi) pi gj (pj c)
+        if (p * C * xi.element_size()) % 8 == 0:
+            # move each patch row segment as 8-byte words: the gi/pj transpose copy runs
+            # 2.3x faster than the element-wise permute (tools/patchbench.py)
+            x = xi.view(torch.int64).transpose(1, 2).contiguous().view(xi.dtype).reshape(B, g * g, p * p * C)
+        else:
+            x = xi.transpose(1, 2).reshape(B, g * g, p * p * C)
         tok = torch.addmm(self.patch_b, x.reshape(-1, x.shape[-1]), self.patch_w).reshape(B, g * g, -1)
         ct = cfg.class_token
         D = tok.shape[-1]
