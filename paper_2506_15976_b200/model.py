@@ -196,6 +196,8 @@ class LBVim:
                 w_outT=cast(w["w_out"]).t().contiguous(),  # "NT" out-projection (~4 % faster)
             ))
         self.head = {k: cast(v) for k, v in params.items() if k.startswith("head.")}
+        # the head runs in fp32 (model.py:238-325); its weights are cast once here, not per forward
+        self.head32 = {k: v.float().contiguous() for k, v in self.head.items()}
         self._graph = None
 
     # -- pieces -----------------------------------------------------------------
@@ -280,14 +282,14 @@ class LBVim:
             nh = cfg.map_heads
             dh = D // nh
             t = tok.float()
-            K = (t @ self.head["head.wk"].float()).reshape(B, L, nh, dh)
-            V = (t @ self.head["head.wv"].float()).reshape(B, L, nh, dh)
-            q = self.head["head.q"].float().reshape(nh, dh)
+            K = (t @ self.head32["head.wk"]).reshape(B, L, nh, dh)
+            V = (t @ self.head32["head.wv"]).reshape(B, L, nh, dh)
+            q = self.head32["head.q"].reshape(nh, dh)
             att = torch.softmax(torch.einsum("blhd,hd->blh", K, q) / math.sqrt(dh), dim=1)
             pooled = torch.einsum("blh,blhd->bhd", att, V).reshape(B, D)
-        h1 = F.gelu(pooled @ self.head["head.mlp_w1"].float() + self.head["head.mlp_b1"].float(),
+        h1 = F.gelu(pooled @ self.head32["head.mlp_w1"] + self.head32["head.mlp_b1"],
                     approximate="tanh")
-        return h1 @ self.head["head.mlp_w2"].float() + self.head["head.mlp_b2"].float()
+        return h1 @ self.head32["head.mlp_w2"] + self.head32["head.mlp_b2"]
 
     @torch.no_grad()
     def forward(self, images):
