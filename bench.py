@@ -210,10 +210,11 @@ def measure_ops(peak, iters=10):
     launching stream, L2 flushed between launches, median of ``iters``."""
     import torch
     sys.path.insert(0, os.path.join(ROOT, "tools"))
-    from kbench import CFGS, alg_bytes, bwd_alg_bytes, make, time_fn
+    from kbench import CFGS, alg_bytes, bwd_alg_bytes, gpu_warmup, make, time_fn
 
     from paper_2506_15976_b200.scan import lbm_selective_scan_bwd, lbm_selective_scan_fwd
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    gpu_warmup()
     names = {"cfg1": "configs[0] op fwd fp32 B=2 E=192 L=197", "cfg2": "configs[1] LBVim-Ti layer scan bf16 B=256 E=384",
              "cfg3": "configs[2] LBVim-S scan fp32 B=128 E=768 fwd+bwd", "cfg4": "configs[3] LBVim-S 1024^2 layer scan bf16 "
              "B=32 L=4096 E=768", "cfg5": "configs[4] MIL bag fp32 B=1 L=100k E=512 (1 GPU)",
