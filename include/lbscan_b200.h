@@ -27,6 +27,7 @@
  *                              nn.causal_conv1d_grad + silu_grad (nn.py:102-114,29-31).
  *   lbs_select_tile_len     <- engine.select_tile_len (engine.py:54-62).
  *   lbs_rms_norm_fwd        <- nn.rms_norm (nn.py:55-58), the block's first op (block.py:170).
+ *   lbs_rms_norm_bwd        <- its adjoint in block_backward (block.py:193-220).
  *
  * Layout: sequence tensors are addressed as element (b, l, e) at
  *   base + b*stride[0] + l*stride[1] + e*stride[2]      (reference: channel-last (B,L,E))
@@ -168,6 +169,26 @@ int lbs_scan_bwd(const lbs_scan_bwd_args* args, void* workspace, size_t workspac
 int lbs_prediscretized_fwd(const lbs_prediscretized_args* args, void* cuda_stream);
 
 int lbs_rms_norm_fwd(const lbs_norm_args* args, void* cuda_stream);
+
+/* RMSNorm backward (the adjoint of nn.rms_norm, nn.py:55-58, as the reference's
+ * block_backward chains it, block.py:193-220): with r = 1/sqrt(mean(x^2) + eps) and
+ * g = dout * scale per row, dx = r g - x r^3 mean(g x); dscale += sum over rows of
+ * dout x r (fp32, fixed-order reduction through the workspace: deterministic).
+ * Any row stride; 16-byte aligned rows with dim <= 128 * (16 / sizeof(elem)) take the
+ * vector kernel. */
+typedef struct lbs_norm_bwd_args {
+  int64_t rows, dim;
+  int32_t io_dtype;
+  float eps;
+  const void* x;     int64_t x_row_stride;
+  const float* scale;         /* (dim) fp32 */
+  const void* dout;  int64_t dout_row_stride;
+  void* dx;          int64_t dx_row_stride;
+  float* dscale;              /* (dim) fp32, accumulated (+=); NULL to skip */
+} lbs_norm_bwd_args;
+size_t lbs_rms_norm_bwd_workspace_bytes(const lbs_norm_bwd_args* args);
+int lbs_rms_norm_bwd(const lbs_norm_bwd_args* args, void* workspace, size_t workspace_bytes,
+                     void* cuda_stream);
 
 size_t lbs_causal_conv1d_bwd_workspace_bytes(const lbs_conv_args* args);
 int lbs_causal_conv1d_fwd(const lbs_conv_args* args, void* cuda_stream);

@@ -88,13 +88,21 @@ class NormArgs(C.Structure):
     ]
 
 
+class NormBwdArgs(C.Structure):
+    _fields_ = [
+        ("rows", I64), ("dim", I64), ("io_dtype", C.c_int32), ("eps", C.c_float),
+        ("x", VP), ("x_row_stride", I64), ("scale", VP), ("dout", VP), ("dout_row_stride", I64),
+        ("dx", VP), ("dx_row_stride", I64), ("dscale", VP),
+    ]
+
+
 # every symbol include/lbscan_b200.h declares (tests check the export table)
 EXPORTS = (
     "lbs_abi_version", "lbs_last_error", "lbs_select_tile_len",
     "lbs_scan_ckpt_len", "lbs_scan_ckpt_bytes",
     "lbs_scan_fwd_workspace_bytes", "lbs_scan_fwd",
     "lbs_scan_bwd_workspace_bytes", "lbs_scan_bwd",
-    "lbs_prediscretized_fwd", "lbs_rms_norm_fwd",
+    "lbs_prediscretized_fwd", "lbs_rms_norm_fwd", "lbs_rms_norm_bwd_workspace_bytes", "lbs_rms_norm_bwd",
     "lbs_causal_conv1d_bwd_workspace_bytes", "lbs_causal_conv1d_fwd", "lbs_causal_conv1d_bwd",
 )
 
@@ -131,6 +139,10 @@ def lib():
     L.lbs_prediscretized_fwd.argtypes = [C.POINTER(PrediscretizedArgs), VP]
     L.lbs_rms_norm_fwd.restype = C.c_int
     L.lbs_rms_norm_fwd.argtypes = [C.POINTER(NormArgs), VP]
+    L.lbs_rms_norm_bwd_workspace_bytes.restype = C.c_size_t
+    L.lbs_rms_norm_bwd_workspace_bytes.argtypes = [C.POINTER(NormBwdArgs)]
+    L.lbs_rms_norm_bwd.restype = C.c_int
+    L.lbs_rms_norm_bwd.argtypes = [C.POINTER(NormBwdArgs), VP, C.c_size_t, VP]
     L.lbs_causal_conv1d_fwd.restype = C.c_int
     L.lbs_causal_conv1d_fwd.argtypes = [C.POINTER(ConvArgs), VP]
     L.lbs_causal_conv1d_bwd_workspace_bytes.restype = C.c_size_t

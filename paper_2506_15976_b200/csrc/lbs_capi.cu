@@ -295,6 +295,35 @@ int lbs_rms_norm_fwd(const lbs_norm_args* a, void* stream) {
   return cuda_status(lbs::launch_rms_norm(p, a->io_dtype, (cudaStream_t)stream), "lbs_rms_norm_fwd");
 }
 
+namespace {
+int validate_norm_bwd(const lbs_norm_bwd_args* a) {
+  if (!a) return fail(LBS_ERR_INVALID, "null args");
+  if (a->rows < 1 || a->dim < 1) return fail(LBS_ERR_INVALID, "rows and dim must be >= 1");
+  if (a->io_dtype != LBS_F32 && a->io_dtype != LBS_BF16) return fail(LBS_ERR_INVALID, "dtype must be f32 or bf16");
+  if (!a->x || !a->scale || !a->dout || !a->dx) return fail(LBS_ERR_INVALID, "null tensor");
+  if (a->dim > (int64_t)1 << 20) return fail(LBS_ERR_UNSUPPORTED, "dim too large");
+  if (a->rows > (int64_t)1 << 34) return fail(LBS_ERR_UNSUPPORTED, "too many rows");
+  return LBS_OK;
+}
+}  // namespace
+
+size_t lbs_rms_norm_bwd_workspace_bytes(const lbs_norm_bwd_args* a) {
+  if (!a || a->rows < 1 || a->dim < 1) return 0;
+  return a->dscale ? (size_t)lbs::norm_bwd_warps(a->rows) * (size_t)a->dim * sizeof(float) : 0;
+}
+
+int lbs_rms_norm_bwd(const lbs_norm_bwd_args* a, void* ws, size_t ws_bytes, void* stream) {
+  const int rc = validate_norm_bwd(a);
+  if (rc != LBS_OK) return rc;
+  const size_t need = lbs_rms_norm_bwd_workspace_bytes(a);
+  if (need && (!ws || ws_bytes < need))
+    return fail(LBS_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+  lbs::NormBwdParams p{a->rows, (int)a->dim, a->eps, a->x, a->x_row_stride, a->scale, a->dout,
+                       a->dout_row_stride, a->dx, a->dx_row_stride, a->dscale, static_cast<float*>(ws),
+                       lbs::norm_bwd_warps(a->rows)};
+  return cuda_status(lbs::launch_rms_norm_bwd(p, a->io_dtype, (cudaStream_t)stream), "lbs_rms_norm_bwd");
+}
+
 size_t lbs_scan_bwd_workspace_bytes(const lbs_scan_bwd_args* a) {
   BwdLayout lay;
   if (bwd_layout(a, &lay) != LBS_OK) return 0;

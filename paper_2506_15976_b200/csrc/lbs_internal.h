@@ -87,4 +87,22 @@ struct NormParams {
 };
 cudaError_t launch_rms_norm(const NormParams& p, int dtype, cudaStream_t st);
 
+struct NormBwdParams {
+  long long rows;
+  int D;
+  float eps;
+  const void* x;
+  long long sx;
+  const float* scale;
+  const void* dout;
+  long long sg;
+  void* dx;
+  long long sdx;
+  float* dscale;
+  float* part;  // (n_warps, D) fp32 dscale partials
+  int n_warps;
+};
+int norm_bwd_warps(long long rows);
+cudaError_t launch_rms_norm_bwd(const NormBwdParams& p, int dtype, cudaStream_t st);
+
 }  // namespace lbs

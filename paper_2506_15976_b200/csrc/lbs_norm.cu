@@ -223,6 +223,185 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Backward.  One warp per row (grid-stride over a fixed set of warps), 16-byte
+// vectors: r is recomputed from x, dot = sum(g x) with g = dout * scale, then
+// dx = r g - x r^3 dot / D.  Each lane keeps its columns' dscale partials
+// (sum of dout x r over the rows it visits) in registers and writes them once
+// per warp; a second kernel adds the per-warp partials in fixed order.
+constexpr int kNormBwdBlocks = 148 * 4;  // x 8 warps (the launch is independent of the device)
+int norm_bwd_warps(long long rows) {
+  const long long w = rows < (long long)kNormBwdBlocks * 8 ? rows : (long long)kNormBwdBlocks * 8;
+  return (int)(w < 1 ? 1 : w);
+}
+
+template <typename T, int VPL>
+__global__ void __launch_bounds__(256) rms_norm_bwd_kernel(NormBwdParams p) {
+  constexpr int EPV = 16 / sizeof(T);
+  const int lane = threadIdx.x % 32;
+  const long long warp = (long long)blockIdx.x * 8 + threadIdx.x / 32;
+  const int D = p.D;
+  float sc[VPL][EPV], dsc[VPL][EPV];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c0 = (lane + 32 * k) * EPV;
+#pragma unroll
+    for (int i = 0; i < EPV; ++i) {
+      sc[k][i] = c0 < D ? p.scale[c0 + i] : 0.f;
+      dsc[k][i] = 0.f;
+    }
+  }
+  const T* X = static_cast<const T*>(p.x);
+  const T* G = static_cast<const T*>(p.dout);
+  T* DX = static_cast<T*>(p.dx);
+  for (long long row = warp; row < p.rows; row += p.n_warps) {
+    float xv[VPL][EPV], gv[VPL][EPV];
+    float ss = 0.f, dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int c0 = (lane + 32 * k) * EPV;
+      uint4 rx = make_uint4(0, 0, 0, 0), rg = make_uint4(0, 0, 0, 0);
+      if (c0 < D) {
+        rx = *reinterpret_cast<const uint4*>(X + row * p.sx + c0);
+        rg = *reinterpret_cast<const uint4*>(G + row * p.sg + c0);
+      }
+      const T* ex = reinterpret_cast<const T*>(&rx);
+      const T* eg = reinterpret_cast<const T*>(&rg);
+#pragma unroll
+      for (int i = 0; i < EPV; ++i) {
+        xv[k][i] = to_f(ex[i]);
+        gv[k][i] = to_f(eg[i]);
+        ss = fmaf(xv[k][i], xv[k][i], ss);
+        dot = fmaf(gv[k][i] * sc[k][i], xv[k][i], dot);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    }
+    const float r = rsqrtf(ss / (float)D + p.eps);
+    const float c = r * r * r * dot / (float)D;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int c0 = (lane + 32 * k) * EPV;
+      if (c0 < D) {
+        uint4 o4;
+        T* e = reinterpret_cast<T*>(&o4);
+#pragma unroll
+        for (int i = 0; i < EPV; ++i) {
+          e[i] = from_f<T>(r * gv[k][i] * sc[k][i] - xv[k][i] * c);
+          dsc[k][i] = fmaf(gv[k][i], xv[k][i] * r, dsc[k][i]);
+        }
+        *reinterpret_cast<uint4*>(DX + row * p.sdx + c0) = o4;
+      }
+    }
+  }
+  if (p.part != nullptr && warp < p.n_warps) {
+    float* pw = p.part + warp * D;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int c0 = (lane + 32 * k) * EPV;
+      if (c0 < D) {
+#pragma unroll
+        for (int i = 0; i < EPV; ++i) pw[c0 + i] = dsc[k][i];
+      }
+    }
+  }
+}
+
+// Any D / alignment: one warp per row, scalar strided accesses; the warp's dscale
+// partial row lives in the workspace (each warp owns its row: no races).
+template <typename T>
+__global__ void __launch_bounds__(256) rms_norm_bwd_scalar_kernel(NormBwdParams p) {
+  const int lane = threadIdx.x % 32;
+  const long long warp = (long long)blockIdx.x * 8 + threadIdx.x / 32;
+  if (warp >= p.n_warps) return;
+  const int D = p.D;
+  const T* X = static_cast<const T*>(p.x);
+  const T* G = static_cast<const T*>(p.dout);
+  T* DX = static_cast<T*>(p.dx);
+  float* pw = p.part ? p.part + warp * D : nullptr;
+  if (pw)
+    for (int c = lane; c < D; c += 32) pw[c] = 0.f;
+  for (long long row = warp; row < p.rows; row += p.n_warps) {
+    float ss = 0.f, dot = 0.f;
+    for (int c = lane; c < D; c += 32) {
+      const float xv = to_f(X[row * p.sx + c]);
+      ss = fmaf(xv, xv, ss);
+      dot = fmaf(to_f(G[row * p.sg + c]) * p.scale[c], xv, dot);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    }
+    const float r = rsqrtf(ss / (float)D + p.eps);
+    const float cc = r * r * r * dot / (float)D;
+    for (int c = lane; c < D; c += 32) {
+      const float xv = to_f(X[row * p.sx + c]);
+      const float gv = to_f(G[row * p.sg + c]);
+      DX[row * p.sdx + c] = from_f<T>(r * gv * p.scale[c] - xv * cc);
+      if (pw) pw[c] = fmaf(gv, xv * r, pw[c]);
+    }
+  }
+}
+
+// dscale[c] += sum over warps of part[w][c]: a 1024-thread block owns 32 columns,
+// 32 slices each sum every 32nd warp's partial (fp64), then the slices are added
+// in fixed order (deterministic; a serial per-column loop over ~4.7k partials was
+// a 350 us load chain)
+__global__ void __launch_bounds__(1024) rms_norm_bwd_reduce_kernel(const float* part, int n_warps, int D,
+                                                                   float* dscale) {
+  __shared__ double acc[32][33];
+  const int lane = threadIdx.x % 32, slice = threadIdx.x / 32;
+  const int c = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (c < D) {
+    int w = slice;
+    for (; w + 96 < n_warps; w += 128) {
+      const float a0 = part[(long long)w * D + c];
+      const float a1 = part[(long long)(w + 32) * D + c];
+      const float a2 = part[(long long)(w + 64) * D + c];
+      const float a3 = part[(long long)(w + 96) * D + c];
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; w < n_warps; w += 32) s += part[(long long)w * D + c];
+  }
+  acc[slice][lane] = s;
+  __syncthreads();
+  if (slice == 0 && c < D) {
+    double t = 0.0;
+    for (int k = 0; k < 32; ++k) t += acc[k][lane];
+    dscale[c] += (float)t;
+  }
+}
+
+template <typename T>
+static cudaError_t launch_norm_bwd_t(const NormBwdParams& p, cudaStream_t st) {
+  constexpr int EPV = 16 / sizeof(T);
+  const int vpl = (p.D / EPV + 31) / 32;
+  const unsigned blocks = (unsigned)((p.n_warps + 7) / 8);
+  auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+  const bool vec = p.D % EPV == 0 && p.sx % EPV == 0 && p.sg % EPV == 0 && p.sdx % EPV == 0 && al(p.x) &&
+                   al(p.dout) && al(p.dx) && vpl <= 4;
+  if (!vec) rms_norm_bwd_scalar_kernel<T><<<blocks, 256, 0, st>>>(p);
+  else if (vpl <= 1) rms_norm_bwd_kernel<T, 1><<<blocks, 256, 0, st>>>(p);
+  else if (vpl <= 2) rms_norm_bwd_kernel<T, 2><<<blocks, 256, 0, st>>>(p);
+  else rms_norm_bwd_kernel<T, 4><<<blocks, 256, 0, st>>>(p);
+  if (p.dscale != nullptr) rms_norm_bwd_reduce_kernel<<<(p.D + 31) / 32, 1024, 0, st>>>(p.part, p.n_warps, p.D, p.dscale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rms_norm_bwd(const NormBwdParams& p, int dtype, cudaStream_t st) {
+  if (dtype == LBS_F32) return launch_norm_bwd_t<float>(p, st);
+  if (dtype == LBS_BF16) return launch_norm_bwd_t<__nv_bfloat16>(p, st);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_rms_norm(const NormParams& p, int dtype, cudaStream_t st) {
   if (dtype == LBS_F32) return launch_norm_t<float>(p, st);
   if (dtype == LBS_BF16) return launch_norm_t<__nv_bfloat16>(p, st);

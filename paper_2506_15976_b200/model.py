@@ -34,7 +34,7 @@ import torch.nn.functional as F
 
 from .conv import causal_conv1d_silu, causal_conv1d_silu_fwd
 from .errors import ShapeError
-from .norm import rms_norm
+from .norm import rms_norm, rms_norm_train
 from .scan import lbm_selective_scan, lbm_selective_scan_fwd
 from .tiling import select_tile_len
 
@@ -335,7 +335,7 @@ def block_forward_train(T, w: dict, M: int, reverse: bool = False, discretize_mo
     RMSNorm and the projections are stock torch autograd.  ``w`` holds the
     reference's weight names (BLOCK_FIELDS).  As in ``LBVim.block`` the output is
     NOT reversed: ``reverse`` selects the scan direction (flip-on-load)."""
-    xn = T * torch.rsqrt(T.float().pow(2).mean(-1, keepdim=True) + eps).to(T.dtype) * w["norm_scale"]
+    xn = rms_norm_train(T, w["norm_scale"], eps)  # fused fwd / bwd kernels
     x = xn @ w["w_x"]
     z = xn @ w["w_z"]
     xs = causal_conv1d_silu(x, w["conv_kernel"], reverse=reverse)

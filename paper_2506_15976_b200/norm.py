@@ -1,4 +1,5 @@
-"""RMSNorm (nn.rms_norm, nn.py:55-58) on the C ABI — the LBVim block's first op."""
+"""RMSNorm (nn.rms_norm, nn.py:55-58) on the C ABI — the LBVim block's first op —
+and its adjoint (block_backward, block.py:193-220) for the training path."""
 
 from __future__ import annotations
 
@@ -31,3 +32,50 @@ def rms_norm(x, scale, eps: float = RMS_EPS, out=None):
     a.out, a.out_row_stride = _ptr(o2), o2.stride(0)
     _lib.check(_lib.lib().lbs_rms_norm_fwd(ctypes.byref(a), _stream()), "rms_norm")
     return out
+
+
+def rms_norm_bwd(x, scale, dout, eps: float = RMS_EPS):
+    """-> (dx in x's dtype, dscale fp32 (D,)).  dx = r g - x r^3 mean(g x) with
+    g = dout * scale, r = 1/sqrt(mean(x^2) + eps); dscale = sum over rows of dout x r
+    (deterministic fixed-order reduction)."""
+    if not x.is_cuda:
+        raise ShapeError("x must be a CUDA tensor (no CPU fallback)")
+    D = x.shape[-1]
+    x2 = x.reshape(-1, D) if x.stride(-1) == 1 else x.contiguous().reshape(-1, D)
+    g2 = dout.to(x.dtype).reshape(-1, D).contiguous()
+    dx = torch.empty_like(x2)
+    dscale = torch.zeros(D, dtype=torch.float32, device=x.device)
+    scale = scale.to(torch.float32).contiguous()
+    a = _lib.NormBwdArgs()
+    a.rows, a.dim, a.io_dtype, a.eps = x2.shape[0], D, _DT[x.dtype], eps
+    a.x, a.x_row_stride = _ptr(x2), x2.stride(0)
+    a.scale = _ptr(scale)
+    a.dout, a.dout_row_stride = _ptr(g2), g2.stride(0)
+    a.dx, a.dx_row_stride = _ptr(dx), dx.stride(0)
+    a.dscale = _ptr(dscale)
+    L = _lib.lib()
+    nws = L.lbs_rms_norm_bwd_workspace_bytes(ctypes.byref(a))
+    ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=x.device)
+    _lib.check(L.lbs_rms_norm_bwd(ctypes.byref(a), ws.data_ptr(), nws, _stream()), "rms_norm_bwd")
+    return dx.reshape(x.shape), dscale
+
+
+class RMSNormFn(torch.autograd.Function):
+    """Fused RMSNorm forward (lbs_rms_norm_fwd) with the fused adjoint (lbs_rms_norm_bwd)."""
+
+    @staticmethod
+    def forward(ctx, x, scale, eps=RMS_EPS):
+        ctx.save_for_backward(x, scale)
+        ctx.eps = eps
+        return rms_norm(x, scale, eps=eps)
+
+    @staticmethod
+    def backward(ctx, dout):
+        x, scale = ctx.saved_tensors
+        dx, ds = rms_norm_bwd(x, scale, dout, eps=ctx.eps)
+        return dx, ds.to(scale.dtype), None
+
+
+def rms_norm_train(x, scale, eps: float = RMS_EPS):
+    """Differentiable RMSNorm on the fused kernels."""
+    return RMSNormFn.apply(x, scale, eps)

@@ -357,3 +357,32 @@ def test_many_segments_prefix(S):
         ref, rhf = O.lbm_selective_scan(**inp, window=16, reverse=reverse, return_last_state=True)
         assert O.max_rel_err(got, ref) <= TOL_F32
         assert O.max_rel_err(hf, rhf) <= TOL_F32
+
+
+@pytest.mark.parametrize("dtype,D", [(torch.float32, 192), (torch.bfloat16, 192), (torch.bfloat16, 384),
+                                     (torch.float32, 64), (torch.bfloat16, 1024), (torch.float32, 6),
+                                     (torch.bfloat16, 50), (torch.float32, 2048)])
+@pytest.mark.parametrize("rows", [1, 3 * 37, 5000])
+def test_rms_norm_bwd(dtype, D, rows):
+    """lbs_rms_norm_bwd against torch autograd of the same formula in fp64 (on the same
+    rounded inputs); dscale accumulated over rows by the fixed-order reduction."""
+    from paper_2506_15976_b200.norm import rms_norm_bwd, rms_norm_train
+    g = torch.Generator(device="cuda").manual_seed(rows + D)
+    x = torch.randn(rows, D, device="cuda", generator=g).to(dtype)
+    s = torch.randn(D, device="cuda", generator=g)
+    dy = torch.randn(rows, D, device="cuda", generator=g).to(dtype)
+    xd = x.double().requires_grad_(True)
+    sd = s.double().requires_grad_(True)
+    y = xd * torch.rsqrt((xd * xd).mean(-1, keepdim=True) + 1e-6) * sd
+    y.backward(dy.double())
+    dx, ds = rms_norm_bwd(x, s, dy)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    assert O.max_rel_err(dx.double().cpu().numpy(), xd.grad.cpu().numpy()) <= tol
+    assert O.max_rel_err(ds.double().cpu().numpy(), sd.grad.cpu().numpy()) <= (1e-5 if dtype == torch.float32 else 1e-3)
+    # deterministic, and the autograd Function routes through the same kernels
+    dx2, ds2 = rms_norm_bwd(x, s, dy)
+    assert torch.equal(dx, dx2) and torch.equal(ds, ds2)
+    xr = x.clone().requires_grad_(True)
+    sr = s.clone().requires_grad_(True)
+    rms_norm_train(xr, sr).backward(dy)
+    assert torch.equal(xr.grad, dx) and torch.equal(sr.grad, ds)
