@@ -336,12 +336,13 @@ def block_forward_train(T, w: dict, M: int, reverse: bool = False, discretize_mo
     reference's weight names (BLOCK_FIELDS).  As in ``LBVim.block`` the output is
     NOT reversed: ``reverse`` selects the scan direction (flip-on-load)."""
     xn = rms_norm_train(T, w["norm_scale"], eps)  # fused fwd / bwd kernels
-    x = xn @ w["w_x"]
-    z = xn @ w["w_z"]
+    E, N = w["w_x"].shape[1], w["w_b"].shape[1]
+    # one GEMM per projection group (x|z and delta|B|C): torch.split's backward
+    # concatenates the slice gradients in one kernel, and under autocast the shared
+    # input is cast once
+    x, z = torch.split(xn @ torch.cat([w["w_x"], w["w_z"]], dim=1), [E, E], dim=-1)
     xs = causal_conv1d_silu(x, w["conv_kernel"], reverse=reverse)
-    delta = xs @ w["w_delta"]
-    Bm = xs @ w["w_b"]
-    Cm = xs @ w["w_c"]
+    delta, Bm, Cm = torch.split(xs @ torch.cat([w["w_delta"], w["w_b"], w["w_c"]], dim=1), [E, N, N], dim=-1)
     A = -torch.exp(w["a_log"].float())
     yg = lbm_selective_scan(xs, delta, A, Bm, Cm, D=w["d_param"], z=z, delta_bias=w["delta_bias"],
                             window=M, reverse=reverse, discretize_mode=discretize_mode, lb=lb)
