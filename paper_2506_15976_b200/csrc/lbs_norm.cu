@@ -254,25 +254,32 @@ __global__ void __launch_bounds__(256) rms_norm_bwd_kernel(NormBwdParams p) {
   const T* X = static_cast<const T*>(p.x);
   const T* G = static_cast<const T*>(p.dout);
   T* DX = static_cast<T*>(p.dx);
-  for (long long row = warp; row < p.rows; row += p.n_warps) {
-    float xv[VPL][EPV], gv[VPL][EPV];
-    float ss = 0.f, dot = 0.f;
+  // the next row's x / dout are loaded before this row is reduced (one row of
+  // loads always in flight per warp)
+  auto load = [&](long long row, uint4 (&rx)[VPL], uint4 (&rg)[VPL]) {
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
       const int c0 = (lane + 32 * k) * EPV;
-      uint4 rx = make_uint4(0, 0, 0, 0), rg = make_uint4(0, 0, 0, 0);
-      if (c0 < D) {
-        rx = *reinterpret_cast<const uint4*>(X + row * p.sx + c0);
-        rg = *reinterpret_cast<const uint4*>(G + row * p.sg + c0);
-      }
-      const T* ex = reinterpret_cast<const T*>(&rx);
-      const T* eg = reinterpret_cast<const T*>(&rg);
+      const bool ok = row < p.rows && c0 < D;
+      rx[k] = ok ? *reinterpret_cast<const uint4*>(X + row * p.sx + c0) : make_uint4(0, 0, 0, 0);
+      rg[k] = ok ? *reinterpret_cast<const uint4*>(G + row * p.sg + c0) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 rx[VPL], rg[VPL];
+  load(warp, rx, rg);
+  for (long long row = warp; row < p.rows; row += p.n_warps) {
+    uint4 nx[VPL], ng[VPL];
+    load(row + p.n_warps, nx, ng);
+    float ss = 0.f, dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const T* ex = reinterpret_cast<const T*>(&rx[k]);
+      const T* eg = reinterpret_cast<const T*>(&rg[k]);
 #pragma unroll
       for (int i = 0; i < EPV; ++i) {
-        xv[k][i] = to_f(ex[i]);
-        gv[k][i] = to_f(eg[i]);
-        ss = fmaf(xv[k][i], xv[k][i], ss);
-        dot = fmaf(gv[k][i] * sc[k][i], xv[k][i], dot);
+        const float xv = to_f(ex[i]);
+        ss = fmaf(xv, xv, ss);
+        dot = fmaf(to_f(eg[i]) * sc[k][i], xv, dot);
       }
     }
 #pragma unroll
@@ -286,15 +293,23 @@ __global__ void __launch_bounds__(256) rms_norm_bwd_kernel(NormBwdParams p) {
     for (int k = 0; k < VPL; ++k) {
       const int c0 = (lane + 32 * k) * EPV;
       if (c0 < D) {
+        const T* ex = reinterpret_cast<const T*>(&rx[k]);
+        const T* eg = reinterpret_cast<const T*>(&rg[k]);
         uint4 o4;
         T* e = reinterpret_cast<T*>(&o4);
 #pragma unroll
         for (int i = 0; i < EPV; ++i) {
-          e[i] = from_f<T>(r * gv[k][i] * sc[k][i] - xv[k][i] * c);
-          dsc[k][i] = fmaf(gv[k][i], xv[k][i] * r, dsc[k][i]);
+          const float xv = to_f(ex[i]), gv = to_f(eg[i]);
+          e[i] = from_f<T>(r * gv * sc[k][i] - xv * c);
+          dsc[k][i] = fmaf(gv, xv * r, dsc[k][i]);
         }
         *reinterpret_cast<uint4*>(DX + row * p.sdx + c0) = o4;
       }
+    }
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      rx[k] = nx[k];
+      rg[k] = ng[k];
     }
   }
   if (p.part != nullptr && warp < p.n_warps) {
@@ -391,6 +406,7 @@ static cudaError_t launch_norm_bwd_t(const NormBwdParams& p, cudaStream_t st) {
   if (!vec) rms_norm_bwd_scalar_kernel<T><<<blocks, 256, 0, st>>>(p);
   else if (vpl <= 1) rms_norm_bwd_kernel<T, 1><<<blocks, 256, 0, st>>>(p);
   else if (vpl <= 2) rms_norm_bwd_kernel<T, 2><<<blocks, 256, 0, st>>>(p);
+  else if (vpl <= 3) rms_norm_bwd_kernel<T, 3><<<blocks, 256, 0, st>>>(p);
   else rms_norm_bwd_kernel<T, 4><<<blocks, 256, 0, st>>>(p);
   if (p.dscale != nullptr) rms_norm_bwd_reduce_kernel<<<(p.D + 31) / 32, 1024, 0, st>>>(p.part, p.n_warps, p.D, p.dscale);
   return cudaGetLastError();
