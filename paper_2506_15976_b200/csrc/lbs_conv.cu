@@ -612,6 +612,124 @@ __global__ void __launch_bounds__(kConvBE) conv_bwd_tile_kernel(ConvParams p) {
   }
 }
 
+// Two-channel variant of the tile backward (whole 128-channel tiles, K = 4, fp32 /
+// bf16): 64 threads, each a channel PAIR with packed taps (FFMA2) and 4-/8-byte
+// shared-memory accesses; per channel the same operation order as
+// conv_bwd_tile_kernel (identical dx and partials).  The one-channel kernel is
+// issue-bound (74 % issue-active, ncu) on per-element index math.
+template <typename T>
+__global__ void __launch_bounds__(64) conv_bwd_tile2_kernel(ConvParams p) {
+  constexpr int KW = 4, K = 4;
+  constexpr int V = 16 / sizeof(T);
+  constexpr int TE = 128, NT = 64, PPR = TE / V;
+  constexpr int TT = kConvChunk;
+  constexpr int XR = TT + 2 * KW;
+  constexpr int GR = TT + KW;
+  __shared__ __align__(16) T xs[XR][TE];
+  __shared__ __align__(16) T gs[GR][TE];
+  T (*dxo)[TE] = gs;  // dx row j overwrites dout row j (consumed K steps earlier)
+  const int e0 = blockIdx.x * TE;
+  const int chunk = blockIdx.y, b = blockIdx.z;
+  const int l0 = chunk * TT;
+  const int L = p.L;
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
+  const T* gb = static_cast<const T*>(p.dout.p) + (long long)b * p.dout.s0 + e0;
+#pragma unroll 4
+  for (int i0 = 0; i0 < (XR + GR) * PPR; i0 += NT) {
+    const int i = i0 + threadIdx.x;
+    const int r = i / PPR, pc = i % PPR;
+    const bool isx = r < XR;
+    const int l = isx ? l0 - (KW - 1) + r : l0 + (r - XR);
+    T* dst = isx ? &xs[r][pc * V] : &gs[r - XR][pc * V];
+    if (l >= 0 && l < L) {
+      const long long ph = rev ? L - 1 - l : l;
+      cp_async16_conv(dst, isx ? xb + ph * p.x.s1 + pc * V : gb + ph * p.dout.s1 + pc * V);
+    } else {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  const int c = 2 * threadIdx.x;
+  const int e = e0 + c;
+  const int l1 = min(L, l0 + TT);
+  auto ld2 = [&](const T* row) -> f2 {
+    if constexpr (sizeof(T) == 4) {
+      const float2 v = *reinterpret_cast<const float2*>(row + c);
+      return mk2(v.x, v.y);
+    } else {
+      const unsigned u = *reinterpret_cast<const unsigned*>(row + c);
+      return mk2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+    }
+  };
+  f2 w[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) w[q] = mk2(p.w[(long long)e * K + q], p.w[(long long)(e + 1) * K + q]);
+  const f2 bias = p.bias ? mk2(p.bias[e], p.bias[e + 1]) : mk2(0.f, 0.f);
+  f2 xw[2 * KW];  // xw[i] = x[l - (KW-1) + i]
+#pragma unroll
+  for (int i = 0; i < 2 * KW; ++i) xw[i] = ld2(xs[i]);  // rows l0-(KW-1)+i -> xs row i
+  auto Gw = [&](int l, int off) -> f2 {
+    if (l + off >= L) return mk2(0.f, 0.f);
+    f2 gv = ld2(gs[l + off - l0]);
+    if (act) {
+      f2 xc = bias;
+#pragma unroll
+      for (int q = 0; q < KW; ++q) xc = fma2(w[q], xw[KW - 1 + off - q], xc);
+      const float s0 = sigmoid_f(xc.x), s1 = sigmoid_f(xc.y);
+      gv.x *= s0 * (1.f + xc.x * (1.f - s0));
+      gv.y *= s1 * (1.f + xc.y * (1.f - s1));
+    }
+    return gv;
+  };
+  f2 dw[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) dw[q] = mk2(0.f, 0.f);
+  f2 db = mk2(0.f, 0.f);
+  f2 fut[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q) fut[q] = Gw(l0, q);
+#pragma unroll 4
+  for (int l = l0; l < l1; ++l) {
+    f2 acc = mk2(0.f, 0.f);
+#pragma unroll
+    for (int q = KW - 1; q >= 0; --q) acc = fma2(w[q], fut[q], acc);
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float2*>(&dxo[l - l0][c]) = make_float2(acc.x, acc.y);
+    } else {
+      *reinterpret_cast<__nv_bfloat162*>(&dxo[l - l0][c]) = __floats2bfloat162_rn(acc.x, acc.y);
+    }
+    const f2 g0 = fut[0];
+    db = add2(db, g0);
+#pragma unroll
+    for (int q = 0; q < KW; ++q) dw[q] = fma2(g0, xw[KW - 1 - q], dw[q]);
+#pragma unroll
+    for (int q = 0; q < KW - 1; ++q) fut[q] = fut[q + 1];
+    fut[K - 1] = Gw(l, K);
+#pragma unroll
+    for (int i = 0; i < 2 * KW - 1; ++i) xw[i] = xw[i + 1];
+    xw[2 * KW - 1] = ld2(xs[l + KW + 1 - l0 + (KW - 1)]);
+  }
+  float* part = p.part + (((long long)b * p.n_chunks + chunk) * p.E + e) * (K + 1);
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    part[q] = dw[q].x;
+    part[(K + 1) + q] = dw[q].y;
+  }
+  part[K] = db.x;
+  part[(K + 1) + K] = db.y;
+  __syncthreads();
+  T* ob = static_cast<T*>(p.dx) + (long long)b * p.sd0 + e0;
+  for (int i = threadIdx.x; i < (l1 - l0) * PPR; i += NT) {
+    const int j = i / PPR, pc = i % PPR;
+    const int l = l0 + j;
+    *reinterpret_cast<uint4*>(ob + (long long)(rev ? L - 1 - l : l) * p.sd1 + pc * V) =
+        *reinterpret_cast<const uint4*>(&dxo[j][pc * V]);
+  }
+}
+
 // deterministic reduction of the (B * n_chunks) partials -> dweight, dbias (+=).
 // A 1024-thread block owns 32 consecutive (e, q) outputs: 32 slices of threads
 // each sum every 32nd partial (fp64, fixed order, 4 loads in flight), then the
@@ -713,7 +831,16 @@ static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
 template <typename T>
 static cudaError_t conv_bwd_t(const ConvParams& p, float* dw, float* db, cudaStream_t st) {
   dim3 grid((p.E + kConvThreads - 1) / kConvThreads, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
-  if (conv_bwd_vec_ok<T>(p) && LBS_CONV_BWD_TILE && p.K == 4) {
+  bool done = false;
+  if constexpr (std::is_same<T, float>::value || std::is_same<T, __nv_bfloat16>::value) {
+    if (conv_bwd_vec_ok<T>(p) && LBS_CONV_BWD_TILE && LBS_CONV_PAIR && p.K == 4 && p.E % 128 == 0) {
+      dim3 gt(p.E / 128, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
+      conv_bwd_tile2_kernel<T><<<gt, 64, 0, st>>>(p);
+      done = true;
+    }
+  }
+  if (done) {
+  } else if (conv_bwd_vec_ok<T>(p) && LBS_CONV_BWD_TILE && p.K == 4) {
     dim3 gt((p.E + kConvBE - 1) / kConvBE, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
     conv_bwd_tile_kernel<T, 4><<<gt, kConvBE, 0, st>>>(p);
   } else if (p.K <= 4) {
