@@ -229,7 +229,7 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
 // dx = r g - x r^3 dot / D.  Each lane keeps its columns' dscale partials
 // (sum of dout x r over the rows it visits) in registers and writes them once
 // per warp; a second kernel adds the per-warp partials in fixed order.
-constexpr int kNormBwdBlocks = 148 * 4;  // x 8 warps (the launch is independent of the device)
+constexpr int kNormBwdBlocks = 148 * 2;  // x 8 warps: one resident wave at 2 blocks/SM (the launch is independent of the device)
 int norm_bwd_warps(long long rows) {
   const long long w = rows < (long long)kNormBwdBlocks * 8 ? rows : (long long)kNormBwdBlocks * 8;
   return (int)(w < 1 ? 1 : w);
