@@ -49,6 +49,9 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 
+#ifndef LBS_DBG_NOMASK
+#define LBS_DBG_NOMASK 0  // test-only: reproduce the pre-fix partial-CTA dB/dC leak
+#endif
 #ifndef LBS_BWD_SIGSTASH
 #define LBS_BWD_SIGSTASH 1  // keep sigmoid(delta_pre), sigmoid(z) from the chunk prologue in shared memory
 #endif
@@ -303,8 +306,10 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
         dAq = fma2(da, bc2(dl[j]), dAq);
         S[j] = fma2(dbx, Bv, S[j]);
         if (x.has_z) Y[j] = fma2(Cv, hr, Y[j]);
-        dBv = mul2(dbx, bc2(dlu[j]));
-        dCv = mul2(hr, bc2(gy[j]));
+        // threads past the last channel (E % 128 != 0) run on unstaged shared-memory
+        // rows: their terms must not enter the block's dB/dC sums (0 * NaN = NaN)
+        dBv = (x.active || LBS_DBG_NOMASK) ? mul2(dbx, bc2(dlu[j])) : mk2(0.f, 0.f);
+        dCv = (x.active || LBS_DBG_NOMASK) ? mul2(hr, bc2(gy[j])) : mk2(0.f, 0.f);
         lam = lamj;
         Qn = Qc;
       }
