@@ -25,6 +25,10 @@ class LbmSelectiveScanFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, u, delta, A, B, C, D, z, delta_bias, delta_softplus, window, reverse, lb,
                 discretize_mode):
+        # parameters given as arrays / lists are tensors from here on (save_for_backward
+        # takes tensors only); their gradients are not returned (no tensor to own them)
+        A, D, delta_bias = (t if t is None or isinstance(t, torch.Tensor) else torch.as_tensor(t, device=u.device)
+                            for t in (A, D, delta_bias))
         out, ck = lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, window,
                                          reverse, False, lb, discretize_mode, save_checkpoints=True)
         ctx.save_for_backward(u, delta, A, B, C, D, z, delta_bias, ck)

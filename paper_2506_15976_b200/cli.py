@@ -1,6 +1,9 @@
-"""Command-line front end mirroring the reference's ``lbscan bench`` and
-``lbscan flops`` (cli/__init__.py:159-218, 326-341) on the B200 kernels.
+"""Command-line front end mirroring the reference's ``lbscan verify``, ``lbscan
+bench`` and ``lbscan flops`` (cli/__init__.py:75-139, 159-218, 326-341) on the
+B200 kernels.
 
+    python -m paper_2506_15976_b200.cli verify [--l 1,5,...] [--m 1,3,...] [--variants forward,lbm,global_bidir]
+                                               [--precision single,double] [--seed 0] [--fused]
     python -m paper_2506_15976_b200.cli bench [--l 4096] [--m 16] [--reps 20] [--ben 65536] [--out f.csv]
     python -m paper_2506_15976_b200.cli flops [--config key=value-file] [--out f.csv]
 
@@ -11,7 +14,11 @@ distribution (cli/__init__.py:143-154), timed with CUDA events on the device
 (inputs resident, interleaved repetitions, median), followed by the same three
 ratio lines.  ``--fused`` adds rows for the fused B200 operator (discretise +
 scan + gate from u/delta/B/C in one launch) at the same B*E*N lanes.
-Exit codes as the reference: 0 ok, 1 runtime/shape error, 2 bad flags.
+``verify`` sweeps the engine against the sequential definition (verify.py) over
+the reference's default grid, fp32 at 1e-5 and fp64 at 1e-12, with bitwise
+equality across repeated launches in place of worker counts; ``--fused`` adds
+the fused operator (both directions).
+Exit codes as the reference: 0 ok, 1 check failure / runtime / shape error, 2 bad flags.
 """
 
 from __future__ import annotations
@@ -99,6 +106,26 @@ def bench_rows(results, L, M, workers):
     return rows
 
 
+def _int_list(text: str) -> list[int]:
+    return [int(tok) for tok in text.split(",") if tok]
+
+
+def cmd_verify(args) -> int:
+    """cli/__init__.py:123-139."""
+    from .verify import TOLERANCE, VerificationError, run_verification
+    try:
+        worst = run_verification(grid_l=args.l, grid_m=args.m, variants=args.variants, precisions=args.precision,
+                                 seed=args.seed, fused=args.fused)
+    except VerificationError as exc:
+        print(f"FAIL: {exc}")
+        return 1
+    for variant, errs in worst.items():
+        for precision, err in errs.items():
+            print(f"{variant:13s} {precision:6s} max rel err {err:.3e}  (tol {TOLERANCE[precision]:.0e})")
+    print("ok")
+    return 0
+
+
 def cmd_bench(args) -> int:
     res = run_bench(args.l, args.m, args.workers, args.reps, ben=args.ben, seed=args.seed, fused=args.fused)
     rows = bench_rows(res, args.l, args.m, args.workers)
@@ -165,6 +192,15 @@ def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="paper_2506_15976_b200.cli", description=__doc__,
                                  formatter_class=argparse.RawDescriptionHelpFormatter)
     sub = ap.add_subparsers(dest="command", required=True)
+    from .verify import DEFAULT_GRID_L, DEFAULT_GRID_M, VARIANTS as VERIFY_VARIANTS
+    p = sub.add_parser("verify", help="engine-vs-sequential equivalence sweep")
+    p.add_argument("--l", type=_int_list, default=list(DEFAULT_GRID_L))
+    p.add_argument("--m", type=_int_list, default=list(DEFAULT_GRID_M))
+    p.add_argument("--variants", type=lambda s: s.split(","), default=list(VERIFY_VARIANTS))
+    p.add_argument("--precision", type=lambda s: s.split(","), default=["single", "double"])
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--fused", action="store_true", help="also verify the fused operator (fp32, both directions)")
+    p.set_defaults(fn=cmd_verify)
     p = sub.add_parser("bench", help="device-timed scan variants + counters (reference CSV schema)")
     p.add_argument("--l", type=int, default=4096)
     p.add_argument("--m", type=int, default=16)
@@ -185,6 +221,16 @@ def build_parser() -> argparse.ArgumentParser:
 def main(argv=None) -> int:
     ap = build_parser()
     args = ap.parse_args(argv)
+    if args.command == "verify":  # cli/__init__.py:398-406
+        from .verify import TOLERANCE, VARIANTS as VV
+        if any(L < 1 for L in args.l) or any(M < 1 for M in args.m):
+            ap.error("--l and --m entries must be >= 1")
+        bad = set(args.variants) - set(VV)
+        if bad:
+            ap.error(f"unknown variants: {sorted(bad)}")
+        bad = set(args.precision) - set(TOLERANCE)
+        if bad:
+            ap.error(f"unknown precisions: {sorted(bad)}")
     if args.command == "bench" and (args.l < 1 or args.m < 1 or args.reps < 1 or args.workers < 1):
         ap.error("--l, --m, --reps and --workers must be >= 1")
     try:

@@ -34,7 +34,19 @@ int cuda_status(cudaError_t e, const char* where) {
 
 bool io_dtype_ok(int d) { return d == LBS_F32 || d == LBS_BF16 || d == LBS_F16; }
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (148 on B200; MIG slices and other SKUs
+// differ), queried once per device ordinal
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int n = cache[dev];
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return n;
+}
 
 // states padded per thread (kernels instantiate NS in {4, 16})
 int padded_states(int64_t N) { return N <= 4 ? 4 : 16; }
@@ -49,16 +61,14 @@ int padded_states(int64_t N) { return N <= 4 ? 4 : 16; }
 void plan_fwd(const lbs_scan_fwd_args* a, int* cta, int* n_seg, int* seg_len) {
   const int64_t L = a->seqlen, m = a->window < a->seqlen ? a->window : a->seqlen;
   const int64_t ctas128 = ((a->dim + 127) / 128) * a->batch;
-  *cta = (a->dim <= 64 || ctas128 < 2 * kNumSMs) ? 64 : 128;
-#ifdef LBS_FORCE_CTA
-  *cta = LBS_FORCE_CTA;  // dev experiments only
-#endif
+  const int sms = num_sms();
+  *cta = (a->dim <= 64 || ctas128 < 2 * sms) ? 64 : 128;
   const int64_t warps = ((a->dim + 31) / 32) * a->batch;
   int64_t S = 1;
   if (a->seg_hint > 0) {
     S = a->seg_hint;
-  } else if (warps < 4 * kNumSMs && L >= 1024) {
-    S = (8 * kNumSMs + warps - 1) / warps;
+  } else if (warps < 4 * sms && L >= 1024) {
+    S = (8 * sms + warps - 1) / warps;
     const int64_t max_s = L / 128;  // segments no shorter than 128 steps
     if (S > max_s) S = max_s;
     if (S > 2048) S = 2048;

@@ -86,165 +86,9 @@ __global__ void __launch_bounds__(kConvThreads) conv_fwd_kernel(ConvParams p) {
   }
 }
 
-// Vectorised forward: one thread = (b, CH-step chunk, V consecutive channels) with
-// V = 16 B / sizeof(T); 16-byte loads/stores of whole channel groups (a warp moves
-// 512 contiguous bytes per row), the K-1 step history in registers, GRP rows of
-// loads issued before use.  Requires E % V == 0, unit channel stride and 16-byte
-// aligned rows (checked by the launcher).
-#ifndef LBS_CONV_SMEM
-// 2: tile kernel (vector in/out, default), 1: smem-in kernel, 0: register kernels.
-// A persistent 2-stage variant of the tile kernel measured 35-50 % slower.
-#define LBS_CONV_SMEM 2
-#endif
-#ifndef LBS_CONV_CHUNK
-#define LBS_CONV_CHUNK 16
-#endif
-#ifndef LBS_CONV_GRP
-#define LBS_CONV_GRP 16
-#endif
-constexpr int kConvVecChunk = LBS_CONV_CHUNK;
-
-template <typename T, int KW>
-__global__ void __launch_bounds__(kConvThreads) conv_fwd_vec_kernel(ConvParams p, int ngroups, int nchunks) {
-  constexpr int V = 16 / sizeof(T);
-  constexpr int GRP = LBS_CONV_GRP;
-  const long long idx = (long long)blockIdx.x * kConvThreads + threadIdx.x;
-  const int g = (int)(idx % ngroups);
-  const long long rest = idx / ngroups;
-  const int chunk = (int)(rest % nchunks);
-  const int b = (int)(rest / nchunks);
-  if (b >= p.Bt) return;
-  const int L = p.L, e0 = g * V;
-  const bool rev = p.flags & LBS_FLAG_REVERSE;
-  const bool act = p.flags & LBS_CONV_SILU;
-  float w[KW][V], bias[V];
-#pragma unroll
-  for (int c = 0; c < V; ++c) {
-#pragma unroll
-    for (int q = 0; q < KW; ++q) w[q][c] = q < p.K ? p.w[(long long)(e0 + c) * p.K + q] : 0.f;
-    bias[c] = p.bias ? p.bias[e0 + c] : 0.f;
-  }
-  const T* xp = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
-  T* op = static_cast<T*>(p.out) + (long long)b * p.so0 + e0;
-  auto phys = [&](int l) -> long long { return rev ? (L - 1 - l) : l; };
-  auto load_row = [&](int l, float (&r)[V]) {
-    if (l >= 0 && l < L) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(xp + phys(l) * p.x.s1);
-      const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-      for (int c = 0; c < V; ++c) r[c] = to_f(e[c]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < V; ++c) r[c] = 0.f;
-    }
-  };
-  const int l0 = chunk * kConvVecChunk;
-  const int l1 = min(L, l0 + kConvVecChunk);
-  float hist[KW][V];  // hist[q] = x[l - q]
-#pragma unroll
-  for (int q = 1; q < KW; ++q) load_row(q < p.K ? l0 - q : -1, hist[q]);
-  for (int l = l0; l < l1; l += GRP) {
-    // GRP rows in flight, kept packed (4 registers each) until their step
-    uint4 raw[GRP];
-#pragma unroll
-    for (int i = 0; i < GRP; ++i)
-      raw[i] = (l + i < l1) ? *reinterpret_cast<const uint4*>(xp + phys(l + i) * p.x.s1) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < GRP; ++i) {
-#pragma unroll
-      for (int q = KW - 1; q >= 1; --q)
-#pragma unroll
-        for (int c = 0; c < V; ++c) hist[q][c] = hist[q - 1][c];
-      const T* xe = reinterpret_cast<const T*>(&raw[i]);
-#pragma unroll
-      for (int c = 0; c < V; ++c) hist[0][c] = to_f(xe[c]);
-      if (l + i < l1) {
-        uint4 raw;
-        T* e = reinterpret_cast<T*>(&raw);
-#pragma unroll
-        for (int c = 0; c < V; ++c) {
-          float acc = bias[c];
-#pragma unroll
-          for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q][c], hist[q][c], acc);
-          const float y = act ? silu_f(acc) : acc;
-          if constexpr (sizeof(T) == 4) e[c] = y;
-          else if constexpr (std::is_same<T, __nv_bfloat16>::value) e[c] = __float2bfloat16_rn(y);
-          else e[c] = __float2half_rn(y);
-        }
-        *reinterpret_cast<uint4*>(op + phys(l + i) * p.so1) = raw;
-      }
-    }
-  }
-}
-
-// Shared-memory staged forward (the default when rows are 16-byte aligned): a
-// CTA owns (b, kConvTileT steps, kConvTileE channels).  Its (T + K - 1) input
-// rows are copied with cp.async 16-byte pieces — every load of the tile in
-// flight at once — then each thread sweeps one channel through the tile from
-// shared memory with the K-1 history in registers.  Flip-on-load: logical row l
-// is physical L-1-l.
-#ifndef LBS_CONV_TILE_T
-#define LBS_CONV_TILE_T 32
-#endif
-constexpr int kConvTileT = LBS_CONV_TILE_T;
-constexpr int kConvTileE = 256;
-
 __device__ __forceinline__ void cp_async16_conv(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-
-template <typename T, int KW>
-__global__ void __launch_bounds__(kConvTileE) conv_fwd_smem_kernel(ConvParams p) {
-  constexpr int V = 16 / sizeof(T);
-  constexpr int ROWS = kConvTileT + KW - 1;
-  __shared__ __align__(16) T tile[ROWS][kConvTileE];
-  const int e0 = blockIdx.x * kConvTileE;
-  const int l0 = blockIdx.y * kConvTileT;
-  const int b = blockIdx.z;
-  const int L = p.L;
-  const int EC = min(kConvTileE, p.E - e0);
-  const bool rev = p.flags & LBS_FLAG_REVERSE;
-  const bool act = p.flags & LBS_CONV_SILU;
-  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
-  // stage rows l0-(KW-1) .. l0+T-1 (logical); out-of-range rows are zero (causal pad)
-  const int pieces_per_row = EC / V;
-  for (int i = threadIdx.x; i < ROWS * pieces_per_row; i += kConvTileE) {
-    const int r = i / pieces_per_row, pc = i - r * pieces_per_row;
-    const int l = l0 - (KW - 1) + r;
-    T* dst = &tile[r][pc * V];
-    if (l >= 0 && l < L) {
-      const long long ph = rev ? (L - 1 - l) : l;
-      cp_async16_conv(dst, xb + ph * p.x.s1 + pc * V);
-    } else {
-      *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-    }
-  }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  const int c = threadIdx.x;
-  if (c >= EC) return;
-  const int e = e0 + c;
-  float w[KW];
-#pragma unroll
-  for (int q = 0; q < KW; ++q) w[q] = q < p.K ? p.w[(long long)e * p.K + q] : 0.f;
-  const float bias = p.bias ? p.bias[e] : 0.f;
-  float hist[KW];  // hist[q] = x[l - q]
-#pragma unroll
-  for (int q = 1; q < KW; ++q) hist[q] = to_f(tile[KW - 1 - q][c]);
-  T* ob = static_cast<T*>(p.out) + (long long)b * p.so0 + (long long)e * p.so2;
-  const int T_ = min(kConvTileT, L - l0);
-#pragma unroll 4
-  for (int j = 0; j < T_; ++j) {
-    hist[0] = to_f(tile[KW - 1 + j][c]);
-    float acc = bias;
-#pragma unroll
-    for (int q = KW - 1; q >= 0; --q) acc = fmaf(w[q], hist[q], acc);
-    const int l = l0 + j;
-    st<T>(ob + (long long)(rev ? (L - 1 - l) : l) * p.so1, act ? silu_f(acc) : acc);
-#pragma unroll
-    for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
-  }
 }
 
 // Tile-staged forward (default for 16-byte aligned rows): a 128-thread CTA owns
@@ -253,16 +97,7 @@ __global__ void __launch_bounds__(kConvTileE) conv_fwd_smem_kernel(ConvParams p)
 // (K-1 history in registers) into an output tile, and the tile leaves as
 // coalesced 16-byte stores -- every HBM access is a whole 16-byte piece.
 // Flip-on-load: logical row l is physical L-1-l for both the input and output.
-#ifndef LBS_CONV_INPLACE
-#define LBS_CONV_INPLACE 1
-#endif
-#ifndef LBS_CONV_PAIR
-#define LBS_CONV_PAIR 1  // two channels per thread for whole 128-channel tiles
-#endif
-#ifndef LBS_CONV_TT
-#define LBS_CONV_TT 32
-#endif
-constexpr int kConvTT = LBS_CONV_TT;
+constexpr int kConvTT = 32;
 constexpr int kConvTE = 128;
 
 template <typename T, int KW>
@@ -349,15 +184,11 @@ __global__ void __launch_bounds__(kConvTE / 2) conv_fwd_tile2_kernel(ConvParams 
   constexpr int PPR = kConvTE / V;     // 16-byte pieces per row
   constexpr int ROWS = kConvTT + KW - 1;
   __shared__ __align__(16) T xin[ROWS][kConvTE];
-#if LBS_CONV_INPLACE
   // output row j overwrites input row j: this thread's columns of row j were
   // last read KW-1 steps earlier (the history lives in registers), and the
   // vector store phase runs after the barrier -- half the shared memory, twice
   // the resident CTAs
   T (*yout)[kConvTE] = xin;
-#else
-  __shared__ __align__(16) T yout[kConvTT][kConvTE];
-#endif
   const int e0 = blockIdx.x * kConvTE;
   const int l0 = blockIdx.y * kConvTT;
   const int b = blockIdx.z;
@@ -512,13 +343,9 @@ __global__ void __launch_bounds__(kConvBE) conv_bwd_tile_kernel(ConvParams p) {
   constexpr int GR = TT + KW;            // dout rows: l0 .. l0+TT+KW-1 (the window's last, unused, lookahead reads row TT+K-1)
   __shared__ __align__(16) T xs[XR][kConvBE];
   __shared__ __align__(16) T gs[GR][kConvBE];
-#if LBS_CONV_INPLACE
   // dx row j overwrites dout row j: this thread last read its column of that row
   // K steps earlier (the g window lives in registers)
   T (*dxo)[kConvBE] = gs;
-#else
-  __shared__ __align__(16) T dxo[TT][kConvBE];
-#endif
   const int e0 = blockIdx.x * kConvBE;
   const int chunk = blockIdx.y, b = blockIdx.z;
   const int l0 = chunk * TT;
@@ -778,9 +605,6 @@ static bool conv_vec_ok(const ConvParams& p) {
          p.x.s1 % V == 0 && p.so0 % V == 0 && p.so1 % V == 0;
 }
 
-#ifndef LBS_CONV_BWD_TILE
-#define LBS_CONV_BWD_TILE 1
-#endif
 template <typename T>
 static bool conv_bwd_vec_ok(const ConvParams& p) {
   constexpr int V = 16 / sizeof(T);
@@ -793,33 +617,17 @@ static bool conv_bwd_vec_ok(const ConvParams& p) {
 template <typename T>
 static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value || std::is_same<T, __nv_bfloat16>::value) {
-    if (conv_vec_ok<T>(p) && LBS_CONV_SMEM == 2 && LBS_CONV_PAIR && p.E % kConvTE == 0) {
+    if (conv_vec_ok<T>(p) && p.E % kConvTE == 0) {
       dim3 grid(p.E / kConvTE, (p.L + kConvTT - 1) / kConvTT, p.Bt);
       if (p.K <= 4) conv_fwd_tile2_kernel<T, 4><<<grid, kConvTE / 2, 0, st>>>(p);
       else conv_fwd_tile2_kernel<T, kMaxWidth><<<grid, kConvTE / 2, 0, st>>>(p);
       return cudaGetLastError();
     }
   }
-  if (conv_vec_ok<T>(p) && LBS_CONV_SMEM == 2) {
+  if (conv_vec_ok<T>(p)) {
     dim3 grid((p.E + kConvTE - 1) / kConvTE, (p.L + kConvTT - 1) / kConvTT, p.Bt);
     if (p.K <= 4) conv_fwd_tile_kernel<T, 4><<<grid, kConvTE, 0, st>>>(p);
     else conv_fwd_tile_kernel<T, kMaxWidth><<<grid, kConvTE, 0, st>>>(p);
-    return cudaGetLastError();
-  }
-  if (conv_vec_ok<T>(p) && LBS_CONV_SMEM) {
-    dim3 grid((p.E + kConvTileE - 1) / kConvTileE, (p.L + kConvTileT - 1) / kConvTileT, p.Bt);
-    if (p.K <= 4) conv_fwd_smem_kernel<T, 4><<<grid, kConvTileE, 0, st>>>(p);
-    else conv_fwd_smem_kernel<T, kMaxWidth><<<grid, kConvTileE, 0, st>>>(p);
-    return cudaGetLastError();
-  }
-  if (conv_vec_ok<T>(p)) {
-    constexpr int V = 16 / sizeof(T);
-    const int ngroups = p.E / V;
-    const int nchunks = (p.L + kConvVecChunk - 1) / kConvVecChunk;
-    const long long units = (long long)p.Bt * nchunks * ngroups;
-    const unsigned blocks = (unsigned)((units + kConvThreads - 1) / kConvThreads);
-    if (p.K <= 4) conv_fwd_vec_kernel<T, 4><<<blocks, kConvThreads, 0, st>>>(p, ngroups, nchunks);
-    else conv_fwd_vec_kernel<T, kMaxWidth><<<blocks, kConvThreads, 0, st>>>(p, ngroups, nchunks);
     return cudaGetLastError();
   }
   dim3 grid((p.E + kConvThreads - 1) / kConvThreads, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
@@ -833,14 +641,14 @@ static cudaError_t conv_bwd_t(const ConvParams& p, float* dw, float* db, cudaStr
   dim3 grid((p.E + kConvThreads - 1) / kConvThreads, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
   bool done = false;
   if constexpr (std::is_same<T, float>::value || std::is_same<T, __nv_bfloat16>::value) {
-    if (conv_bwd_vec_ok<T>(p) && LBS_CONV_BWD_TILE && LBS_CONV_PAIR && p.K == 4 && p.E % 128 == 0) {
+    if (conv_bwd_vec_ok<T>(p) && p.K == 4 && p.E % 128 == 0) {
       dim3 gt(p.E / 128, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
       conv_bwd_tile2_kernel<T><<<gt, 64, 0, st>>>(p);
       done = true;
     }
   }
   if (done) {
-  } else if (conv_bwd_vec_ok<T>(p) && LBS_CONV_BWD_TILE && p.K == 4) {
+  } else if (conv_bwd_vec_ok<T>(p) && p.K == 4) {
     dim3 gt((p.E + kConvBE - 1) / kConvBE, (p.L + kConvChunk - 1) / kConvChunk, p.Bt);
     conv_bwd_tile_kernel<T, 4><<<gt, kConvBE, 0, st>>>(p);
   } else if (p.K <= 4) {

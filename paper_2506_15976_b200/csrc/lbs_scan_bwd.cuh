@@ -28,18 +28,14 @@
 // recomputes a, h and the LB adjoint v in registers, and a descending pass
 // runs the LB record r (as Q = r + b), the global adjoint lam and all chain
 // terms with packed FFMA2.  lam crosses chunk boundaries through shared
-// memory.  The E-reductions for dB/dC are a warp reduce-scatter (16 values
-// per 16 shuffles) + a 4-warp smem sum, written as per-CTA partials and
+// memory.  The E-reductions for dB/dC are a per-warp shared-memory transpose
+// (one 16-byte store per step, fixed-order lane sums) + a 4-warp sum, written as per-CTA partials and
 // reduced deterministically by a second kernel (no atomics: the reference's
 // partial-then-reduce order, autodiff.py:182,188).
 #pragma once
 #include "lbs_scan_fwd.cuh"
 
 namespace lbs {
-
-#ifndef LBS_BWD_RED_SMEM
-#define LBS_BWD_RED_SMEM 1  // dB/dC warp sums by shared-memory transpose (else shuffle reduce-scatter)
-#endif
 
 constexpr int kBwdThreads = kFwdThreads;  // BcPrefetch assumes 128 threads
 constexpr float kLn2 = 0.6931471805599453f;
@@ -49,12 +45,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
 
-#ifndef LBS_DBG_NOMASK
-#define LBS_DBG_NOMASK 0  // test-only: reproduce the pre-fix partial-CTA dB/dC leak
-#endif
-#ifndef LBS_BWD_SIGSTASH
-#define LBS_BWD_SIGSTASH 1  // keep sigmoid(delta_pre), sigmoid(z) from the chunk prologue in shared memory
-#endif
 
 template <typename Tio, int NS, int KT>
 struct BwdSmem {
@@ -76,7 +66,7 @@ struct BwdSmem {
   static constexpr size_t off_tr = off_raw + raw_bytes;
   // sigmoid(delta_pre) and sigmoid(z) of the chunk's steps, kept from the
   // prologue (which already has e^x / computes silu(z)) for the epilogue
-  static constexpr size_t sig_bytes = LBS_BWD_SIGSTASH ? 2ull * KT * kBwdThreads * sizeof(float) : 0;
+  static constexpr size_t sig_bytes = 2ull * KT * kBwdThreads * sizeof(float);
   static constexpr size_t off_sig = off_tr + tr_bytes;
   static constexpr size_t total = off_sig + sig_bytes;
 };
@@ -130,39 +120,6 @@ struct BwdStager {
   }
 };
 
-// Warp reduce-scatter of 16 values: returns, in lane l, the warp sum of value
-// index (l >> 1) (lanes l and l^1 hold the same sum).  16 shuffles total.
-__device__ __forceinline__ float reduce_scatter16(float (&v)[16], int lane) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool hi = lane & 16;
-    const float send = hi ? v[i] : v[i + 8];
-    const float keep = hi ? v[i + 8] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const bool hi = lane & 8;
-    const float send = hi ? v[i] : v[i + 4];
-    const float keep = hi ? v[i + 4] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const bool hi = lane & 4;
-    const float send = hi ? v[i] : v[i + 2];
-    const float keep = hi ? v[i + 2] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  {
-    const bool hi = lane & 2;
-    const float send = hi ? v[0] : v[1];
-    const float keep = hi ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
-
 struct BwdChunkCtx {
   int c, clen, L, m, stg;
   unsigned tstart, tend;  // bit j: step j starts / ends an LB tile
@@ -195,7 +152,6 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
   }
   // one uniform branch per chunk for each of softplus and the gate: the
   // per-step MUFU chains are independent and interleave
-#if LBS_BWD_SIGSTASH
   float* sig_d = sig;                      // [KT][128]: sigmoid(delta + bias)
   float* sig_z = sig + KT * kBwdThreads;   // [KT][128]: sigmoid(z)
   if (x.softplus) {
@@ -223,18 +179,6 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
       }
     }
   }
-#else
-  (void)sig;
-  if (x.softplus) {
-#pragma unroll
-    for (int j = 0; j < KT; ++j) dl[j] = softplus_f(dl[j]);
-  }
-  if (x.has_z) {
-#pragma unroll
-    for (int j = 0; j < KT; ++j)
-      if (kFull || j < clen) gy[j] *= silu_f(to_f(sz[j * kBwdThreads + tid]));
-  }
-#endif
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
     if (!(kFull || j < clen)) dl[j] = 0.f;
@@ -278,7 +222,6 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
     }
     // ---- descending: LB record Q = r + b, adjoint lam, chain terms
     f2 Qn = mk2(0.f, 0.f), lam = mk2(0.f, 0.f), dAq = mk2(0.f, 0.f);
-    float rv[16];
 #pragma unroll
     for (int j = KT - 1; j >= 0; --j) {
       f2 dBv = mk2(0.f, 0.f), dCv = mk2(0.f, 0.f);
@@ -308,35 +251,16 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
         if (x.has_z) Y[j] = fma2(Cv, hr, Y[j]);
         // threads past the last channel (E % 128 != 0) run on unstaged shared-memory
         // rows: their terms must not enter the block's dB/dC sums (0 * NaN = NaN)
-        dBv = (x.active || LBS_DBG_NOMASK) ? mul2(dbx, bc2(dlu[j])) : mk2(0.f, 0.f);
-        dCv = (x.active || LBS_DBG_NOMASK) ? mul2(hr, bc2(gy[j])) : mk2(0.f, 0.f);
+        dBv = x.active ? mul2(dbx, bc2(dlu[j])) : mk2(0.f, 0.f);
+        dCv = x.active ? mul2(hr, bc2(gy[j])) : mk2(0.f, 0.f);
         lam = lamj;
         Qn = Qc;
       }
-#if LBS_BWD_RED_SMEM
-      // park the 4 values of step j in this warp's transpose buffer [v][lane]
       // this lane's row [lane][v] of the warp's transpose buffer, row stride KT*4+4
       // (= 4 mod 32: the 16-byte stores of a quarter-warp hit distinct banks)
       float* tw = tr + (size_t)warp * 32 * (KT * 4 + 4);
       *reinterpret_cast<float4*>(&tw[lane * (KT * 4 + 4) + j * 4]) = make_float4(dBv.x, dBv.y, dCv.x, dCv.y);
-      (void)rv;
-#else
-      const int o = (j & 3) * 4;
-      rv[o + 0] = dBv.x;
-      rv[o + 1] = dBv.y;
-      rv[o + 2] = dCv.x;
-      rv[o + 3] = dCv.y;
-      if ((j & 3) == 0) {
-        const float s = reduce_scatter16(rv, lane);
-        if ((lane & 1) == 0) {
-          const int idx = lane >> 1;
-          const int jj = j + (idx >> 2), kind = idx & 3;
-          red[((warp * KT + jj) * 2 + (kind >> 1)) * NS + 2 * q + (kind & 1)] = s;
-        }
-      }
-#endif
     }
-#if LBS_BWD_RED_SMEM
     // warp sum of each of the KT*4 values: lane l owns values l, l+32, ...
     __syncwarp();
     {
@@ -357,7 +281,6 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
       }
     }
     __syncwarp();
-#endif
     // carry into the previous chunk: a_{c} * lam_{c}
     mu[q * kBwdThreads + tid] = mul2(a[0], lam);
     dAs[q * kBwdThreads + tid] = add2(dAs[q * kBwdThreads + tid], dAq);
@@ -376,12 +299,7 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
         const float duv = x.Dv * gy[j] + dl[j] * s;
         const float pp = (Pacc[j].x + Pacc[j].y) * (x.linear ? 1.f : kLn2);
         const float ddl = pp + uv * s;
-#if LBS_BWD_SIGSTASH
         const float ddv = x.softplus ? ddl * sig_d[j * kBwdThreads + tid] : ddl;
-#else
-        const float dpre = to_f(sd[j * kBwdThreads + tid]) + x.bias;
-        const float ddv = x.softplus ? ddl * sigmoid_f(dpre) : ddl;
-#endif
         dbias_acc += ddv;
         dD_acc += gy[j] * uv;
         st<Tio>(dupj, duv);
@@ -389,11 +307,7 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
         if (x.has_z) {
           const float y = Y[j].x + Y[j].y + x.Dv * uv;
           const float zv = to_f(sz[j * kBwdThreads + tid]);
-#if LBS_BWD_SIGSTASH
           const float sgm = sig_z[j * kBwdThreads + tid];
-#else
-          const float sgm = sigmoid_f(zv);
-#endif
           const float go = to_f(sg[j * kBwdThreads + tid]);
           st<Tio>(dzpj, go * y * sgm * (1.f + zv * (1.f - sgm)));
         }
@@ -473,7 +387,7 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
   const View3D views[4] = {p.u, p.delta, zv, P.dout};
   BwdStager<Tio, kVec, KT> stager;
   stager.init(views, L, rev, b, e0, p.E);
-  BcStage<Tbc, NS, KT, kVec, true> bcs;  // interleaved fp32 table, cp.async when aligned
+  BcStage<Tbc, NS, KT, kVec && bc_async_ok<Tbc, NS>(), true> bcs;  // interleaved fp32 table, cp.async when aligned
   bcs.init(p, b);
   const bool one_tile = m == KT;
   const f2* ckg = reinterpret_cast<const f2*>(p.ckpt) + (long long)b * nck * NP * p.E + ec;
@@ -647,9 +561,7 @@ inline cudaError_t launch_bwd_v(const BwdParams& P, cudaStream_t st) {
     return v.s2 == 1 && (reinterpret_cast<uintptr_t>(v.p) % 16) == 0 && (v.s0 * es) % 16 == 0 &&
            (v.s1 * es) % 16 == 0;
   };
-  const size_t eb = sizeof(Tbc);
-  const int NS = P.f.N <= 4 ? 4 : 16;
-  const bool bc = P.f.N == NS && view_vec_ok(P.f.Bm, eb) && view_vec_ok(P.f.Cm, eb) && P.f.Bm.s1 == P.f.Cm.s1;
+  const bool bc = bc_vec_ok<Tbc>(P.f);
   const bool vec = P.f.E % epp == 0 && ok(P.f.u) && ok(P.f.delta) && ok(P.f.z) && ok(P.dout) && bc;
   return vec ? launch_bwd_n<Tio, Tbc, true>(P, st) : launch_bwd_n<Tio, Tbc, false>(P, st);
 }

@@ -129,9 +129,8 @@ struct SeqStager {
 // B/C of one chunk: each thread owns one fixed (B|C, n) column and rows
 // t = row0 + k*RS; values are prefetched into registers one chunk ahead and
 // published to shared memory as fp32 (zero for n >= N).
-#ifndef LBS_BC_IL
-#define LBS_BC_IL 1  // forward B/C table layout: [t][pair q][B0 B1 C0 C1] (one LDS.128 per pair-step)
-#endif
+// forward B/C table layout: [t][pair q][B0 B1 C0 C1] (one LDS.128 per pair-step)
+constexpr bool kBcIL = true;
 // index of (step t, B|C = w, state n) in the fp32 broadcast table
 template <int NS, bool kIL>
 __host__ __device__ constexpr int bc_index(int t, int w, int n) {
@@ -180,6 +179,11 @@ struct BcPrefetch {
   }
 };
 
+// B/C rows can go through 16-byte cp.async only when a row of NS elements is
+// whole 16-byte pieces (not bf16 with NS = 4: 8 bytes per row)
+template <typename Tbc, int NS>
+__host__ __device__ constexpr bool bc_async_ok() { return (NS * sizeof(Tbc)) % 16 == 0; }
+
 // B/C staging for one chunk.  kAsync (N == NS, rows of 16-byte pieces): the
 // raw rows are copied by cp.async into a 2-stage shared-memory ring together
 // with u/delta/z — a global load the compiler cannot sink to its use — and
@@ -188,6 +192,7 @@ template <typename Tbc, int NS, int CL, bool kAsync, bool kIL = false, int CT = 
 struct BcStage {
   static constexpr int EPB = 16 / sizeof(Tbc);   // elements per 16-byte piece
   static constexpr int PB = NS / EPB;            // pieces per B (or C) row
+  static_assert(!kAsync || (PB >= 1 && PB * EPB == NS), "async B/C rows must be whole 16-byte pieces");
   BcPrefetch<Tbc, NS, CL, kIL, CT> pre;
   const Tbc* base[2];
   long long step;
@@ -232,10 +237,6 @@ struct BcStage {
   }
 };
 
-#ifndef LBS_QTRICK
-#define LBS_QTRICK 0
-#endif
-
 // One LB tile of r steps at ring rows [t0, t0+r): all state pairs, then the
 // D-skip + gate + store.  For MT > 8 the injections b_j are recomputed in the
 // forward sweep instead of held (keeps the 16-step window under 168 regs).
@@ -248,19 +249,6 @@ struct TileOut {
   bool accum;      // out += y (LBS_FLAG_ACCUM)
 };
 
-#ifndef LBS_DBG_NOEXP
-#define LBS_DBG_NOEXP 0
-#endif
-#ifndef LBS_DBG_NOSOFTPLUS
-#define LBS_DBG_NOSOFTPLUS 0
-#endif
-#ifndef LBS_DBG_NOSTORE
-#define LBS_DBG_NOSTORE 0
-#endif
-
-#ifndef LBS_SP_HOIST
-#define LBS_SP_HOIST 1
-#endif
 #ifndef LBS_RAGGED_QU
 #define LBS_RAGGED_QU 2  // state pairs per unrolled group in the LB ragged-tile path (-2..4 % vs 1)
 #endif
@@ -273,24 +261,16 @@ struct TileOut {
 
 // One state pair (n, n+1) through one tile: exps, tile-local record, forward
 // recurrence, accumulation of C (h + r) into the per-step outputs.
-#ifndef LBS_HOLDC
-#define LBS_HOLDC 1  // with the interleaved table: one LDS.128 per pair-step, C held in registers
-#endif
-
-template <int NS, int MT, bool kLB, bool kFull, bool kIL = LBS_BC_IL>
+template <int NS, int MT, bool kLB, bool kFull, bool kIL = kBcIL>
 __device__ __forceinline__ void pair_tile(f2& hq, const f2 A2, int q, const float (&dl)[MT], const float (&du)[MT],
                                           f2 (&yacc)[MT], const float* bcf, int t0, int r, bool linear) {
   constexpr bool kHoldB = MT <= 8;
-  constexpr bool kHoldC = kIL && kHoldB && LBS_HOLDC;
+  constexpr bool kHoldC = kIL && kHoldB;  // interleaved table: one LDS.128 per pair-step, C held
   f2 a[MT], bb[kHoldB ? MT : 1], cc[kHoldC ? MT : 1];
 #pragma unroll
   for (int j = 0; j < MT; ++j) {
     const f2 x = mul2(bc2(dl[j]), A2);
-#if LBS_DBG_NOEXP  // ablation only: no MUFU for the state decays
-    a[j] = fma2(x, bc2(0.01f), bc2(0.9f));
-#else
     a[j] = linear ? x : mk2(ex2(x.x), ex2(x.y));
-#endif
     if constexpr (kHoldC) {
       const float4 v = *reinterpret_cast<const float4*>(&bcf[bc_index<NS, true>(t0 + j, 0, 2 * q)]);
       bb[j] = mul2(bc2(du[j]), mk2(v.x, v.y));
@@ -315,31 +295,6 @@ __device__ __forceinline__ void pair_tile(f2& hq, const f2 A2, int q, const floa
       return *reinterpret_cast<const f2*>(&bcf[bc_index<NS, kIL>(t0 + j, 1, 2 * q)]);
     }
   };
-#if LBS_QTRICK
-  if (kLB) {
-    // LB record as Q_i = r_i + b_i = a_i Q_{i+1} + b_i (Q = b at a tile end), so
-    // h_i + r_i = a_i h_{i-1} + Q_i: one FFMA2 per step on the right-to-left chain.
-    // At tile ends Q = b, so h + r is the forward state bit for bit.
-    f2 Q[MT];
-#pragma unroll
-    for (int j = MT - 1; j >= 0; --j) {
-      if (kFull ? (j == MT - 1) : (j == r - 1)) {
-        Q[j] = binj(j);
-      } else if (kFull || j < r - 1) {
-        Q[j] = fma2(a[j], Q[j < MT - 1 ? j + 1 : j], binj(j));
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < MT; ++j) {
-      if (kFull || j < r) {
-        const f2 hr = fma2(a[j], hq, Q[j]);
-        hq = fma2(a[j], hq, binj(j));
-        yacc[j] = fma2(cinj(j), hr, yacc[j]);
-      }
-    }
-    return;
-  }
-#endif
   if (kLB) {
     // exclusive tile-local backward record: r_{end} = 0, r_i = a_i (r_{i+1} + b_{i+1})
     f2 s = mk2(0.f, 0.f);
@@ -371,48 +326,6 @@ __device__ __forceinline__ void pair_tile(f2& hq, const f2 A2, int q, const floa
       hq = fma2(a[j], hq, binj(j));
       yacc[j] = fma2(cinj(j), hq, yacc[j]);
     }
-  }
-}
-
-#ifndef LBS_PIPE
-#define LBS_PIPE 0  // software-pipeline the state-pair loop: next pair's EX2s under this pair's chains
-#endif
-
-// Software-pipelined pieces of pair_tile for full tiles with MT <= 8: the
-// decays of pair q+1 (MUFU) are issued while the dependent FFMA2 chains of
-// pair q run, so one warp feeds both pipes (the plain loop issues them in turns).
-template <int NS, int MT>
-__device__ __forceinline__ void pair_exps(f2 (&a)[MT], const f2 A2, const float (&dl)[MT], bool linear) {
-#pragma unroll
-  for (int j = 0; j < MT; ++j) {
-    const f2 x = mul2(bc2(dl[j]), A2);
-    a[j] = linear ? x : mk2(ex2(x.x), ex2(x.y));
-  }
-}
-
-template <int NS, int MT, bool kLB>
-__device__ __forceinline__ void pair_chains(f2& hq, const f2 (&a)[MT], int q, const float (&du)[MT],
-                                            f2 (&yacc)[MT], const float* bcf, int t0) {
-  f2 bb[MT], cc[MT];
-#pragma unroll
-  for (int j = 0; j < MT; ++j) {
-    const float4 v = *reinterpret_cast<const float4*>(&bcf[bc_index<NS, true>(t0 + j, 0, 2 * q)]);
-    bb[j] = mul2(bc2(du[j]), mk2(v.x, v.y));
-    cc[j] = mk2(v.z, v.w);
-  }
-  if (kLB) {
-    f2 s = bb[MT - 1];
-#pragma unroll
-    for (int j = MT - 2; j >= 0; --j) {
-      const f2 rr = mul2(a[j], s);
-      yacc[j] = fma2(cc[j], rr, yacc[j]);
-      s = add2(rr, bb[j]);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < MT; ++j) {
-    hq = fma2(a[j], hq, bb[j]);
-    yacc[j] = fma2(cc[j], hq, yacc[j]);
   }
 }
 
@@ -461,20 +374,12 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
     dl[j] = on ? to_f(sd[(t0 + j) * CT + tid]) + bias : 0.f;
     uv[j] = on ? to_f(su[(t0 + j) * CT + tid]) : 0.f;
   }
-#if !LBS_DBG_NOSOFTPLUS
-#if LBS_SP_HOIST
   // one uniform branch per tile: the MT softplus chains (EX2 -> LG2) are
   // independent and interleave
   if (softplus) {
 #pragma unroll
     for (int j = 0; j < MT; ++j) dl[j] = softplus_f(dl[j]);
   }
-#else
-#pragma unroll
-  for (int j = 0; j < MT; ++j)
-    if (softplus) dl[j] = softplus_f(dl[j]);
-#endif
-#endif
 #pragma unroll
   for (int j = 0; j < MT; ++j) {
     du[j] = dl[j] * uv[j];
@@ -484,25 +389,6 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 #pragma unroll
     for (int q = 0; q < NP; ++q)
       pair_tile<NS, MT, kLB, kFull>(h.r[q], a2s[q * CT + tid], q, dl, du, yacc, bcf, t0, r, linear);
-  } else if constexpr (LBS_PIPE && kFull && MT <= 8 && LBS_BC_IL && NP % 2 == 0) {
-    // two-stage pipeline over state pairs, unrolled by 2 so the buffers swap names
-    f2 aA[MT], aB[MT];
-    pair_exps<NS, MT>(aA, a2s[tid], dl, linear);
-#pragma unroll 1
-    for (int q = 0; q < NP; q += 2) {
-      pair_exps<NS, MT>(aB, a2s[(q + 1) * CT + tid], dl, linear);
-      {
-        f2 hq = h.get(q);
-        pair_chains<NS, MT, kLB>(hq, aA, q, du, yacc, bcf, t0);
-        h.set(q, hq);
-      }
-      if (q + 2 < NP) pair_exps<NS, MT>(aA, a2s[(q + 2) * CT + tid], dl, linear);
-      {
-        f2 hq = h.get(q + 1);
-        pair_chains<NS, MT, kLB>(hq, aB, q + 1, du, yacc, bcf, t0);
-        h.set(q + 1, hq);
-      }
-    }
   } else {
 #pragma unroll 1
     for (int q0 = 0; q0 < NP; q0 += QU) {
@@ -521,13 +407,9 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
     for (int j = 0; j < MT; ++j) {
       if (j < r) {
         float y = yacc[j].x + yacc[j].y;
-#if LBS_DBG_NOSTORE  // ablation only
-        if (y == 1234.5f) st<Tio>(dst, y);
-#else
         if (o.has_z) y *= silu_out<Tio>(to_f(sz[(t0 + j) * CT + tid]));
         if constexpr (kAccum) y += prev[j];
         st<Tio>(dst, y);
-#endif
       }
       dst += o.step;
     }
@@ -539,9 +421,6 @@ constexpr int fwd_chunk(int mt) { return mt > LBS_FWD_CL ? mt : LBS_FWD_CL; }
 
 #ifndef LBS_FWD_MINB
 #define LBS_FWD_MINB 4
-#endif
-#ifndef LBS_BC_ASYNC
-#define LBS_BC_ASYNC 1
 #endif
 #ifndef LBS_FWD_MINB16
 #define LBS_FWD_MINB16 2
@@ -607,7 +486,7 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
 
   SeqStager<Tio, kVec, CL, CT> stager;
   stager.init(p, b, e0, has_z);
-  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL, CT> bcs;
+  BcStage<Tbc, NS, CL, kVec && bc_async_ok<Tbc, NS>(), kBcIL, CT> bcs;
   bcs.init(p, b);
   // prologue: chunk 0
   int c = seg_lo;
@@ -719,7 +598,7 @@ __global__ void __launch_bounds__(CT) segment_state_kernel(FwdParams p) {
 
   SeqStager<Tio, kVec, LBS_FWD_CL, CT> stager;
   stager.init(p, b, e0, false);
-  BcStage<Tbc, NS, CL, kVec && LBS_BC_ASYNC, LBS_BC_IL, CT> bcs;
+  BcStage<Tbc, NS, CL, kVec && bc_async_ok<Tbc, NS>(), kBcIL, CT> bcs;
   bcs.init(p, b);
   int c = seg_lo;
   int clen = min(CL, seg_hi - c);
@@ -750,7 +629,7 @@ __global__ void __launch_bounds__(CT) segment_state_kernel(FwdParams p) {
       for (int q = 0; q < NP; ++q) {
         const f2 x = mul2(bc2(dl), a2s[q * CT + tid]);
         const f2 a = linear ? x : mk2(ex2(x.x), ex2(x.y));
-        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[bc_index<NS, LBS_BC_IL>(t, 0, 2 * q)]);
+        const f2 Bv = *reinterpret_cast<const f2*>(&bcf[bc_index<NS, kBcIL>(t, 0, 2 * q)]);
         H[q] = fma2(a, H[q], mul2(bc2(du), Bv));
         if (linear) P[q] = mul2(P[q], a);
       }
@@ -900,13 +779,24 @@ inline bool view_vec_ok(const View3D& v, size_t es) {
          (v.s1 * es) % 16 == 0;
 }
 
+// kVec also selects cp.async B/C staging when bc_async_ok<Tbc, NS>(); the B/C
+// rows must then be N == NS aligned pieces with equal row strides (else the
+// register-prefetch B/C path, which takes any layout, runs with kVec rows)
+template <typename Tbc>
+inline bool bc_vec_ok(const FwdParams& p) {
+  const size_t eb = sizeof(Tbc);
+  const int NS = p.N <= 4 ? 4 : 16;
+  const bool async = NS == 4 ? bc_async_ok<Tbc, 4>() : bc_async_ok<Tbc, 16>();
+  if (!async) return true;
+  return p.N == NS && view_vec_ok(p.Bm, eb) && view_vec_ok(p.Cm, eb) && p.Bm.s1 == p.Cm.s1;
+}
+
 template <typename Tio, typename Tbc>
 static bool vec_ok(const FwdParams& p) {
-  const size_t es = sizeof(Tio), eb = sizeof(Tbc);
+  const size_t es = sizeof(Tio);
   const int epp = 16 / (int)es;
-  const int NS = p.N <= 4 ? 4 : 16;
-  const bool bc = p.N == NS && view_vec_ok(p.Bm, eb) && view_vec_ok(p.Cm, eb) && p.Bm.s1 == p.Cm.s1;
-  return p.E % epp == 0 && view_vec_ok(p.u, es) && view_vec_ok(p.delta, es) && view_vec_ok(p.z, es) && bc;
+  return p.E % epp == 0 && view_vec_ok(p.u, es) && view_vec_ok(p.delta, es) && view_vec_ok(p.z, es) &&
+         bc_vec_ok<Tbc>(p);
 }
 
 template <typename Tio, typename Tbc>

@@ -94,8 +94,18 @@ def lbm_scan_par_reverse(abar, bx, c, dx, plan: TilePlan, workers: int = 1) -> S
     return _run(abar, bx, c, dx, plan, workers, True, True, "lbm")
 
 
+def _fields(p):
+    """(abar, bx, c, dx) of a reference ``core.ScanParams`` (a plain dataclass,
+    core.py:89-108) or of any 4-sequence."""
+    if hasattr(p, "abar"):
+        return p.abar, p.bx, p.c, p.dx
+    return tuple(p)
+
+
 def global_bidir_par(params_f, params_b, plan: TilePlan, workers: int = 1) -> ScanOutput:
-    """engine.py:305-327: two full sweeps (the second flip-on-load), summed."""
-    f = _run(*params_f, plan, workers, False, False, "global_bidir")
-    b = _run(*params_b, plan, workers, False, True, "global_bidir")
+    """engine.py:305-327: two full sweeps (the second flip-on-load), summed.
+    ``params_f`` / ``params_b`` are ``ScanParams`` like the reference's
+    (test_engine.py:64,73) or (abar, bx, c, dx) tuples."""
+    f = _run(*_fields(params_f), plan, workers, False, False, "global_bidir")
+    b = _run(*_fields(params_b), plan, workers, False, True, "global_bidir")
     return ScanOutput(y=f.y + b.y, h_final=f.h_final + b.h_final, cost=f.cost + b.cost)

@@ -270,23 +270,7 @@ class LBVim:
         reference reads class tokens at p or L-1-p depending on how many
         reversals are left (model.py:225-229,307-312) — both are original
         position p — and its GAP / MAP pools are order-invariant."""
-        cfg = self.cfg
-        ct = cfg.class_token
-        if ct != "none":
-            pos = {"head": [0], "middle": [cfg.num_patches // 2], "double": [0, cfg.seq_len - 1]}[ct]
-            pooled = torch.stack([tok[:, q] for q in pos], 1).float().mean(1)  # graph-capturable
-        elif cfg.head == "gap":
-            pooled = tok.float().mean(1)
-        else:
-            B, L, D = tok.shape
-            nh = cfg.map_heads
-            dh = D // nh
-            t = tok.float()
-            K = (t @ self.head32["head.wk"]).reshape(B, L, nh, dh)
-            V = (t @ self.head32["head.wv"]).reshape(B, L, nh, dh)
-            q = self.head32["head.q"].reshape(nh, dh)
-            att = torch.softmax(torch.einsum("blhd,hd->blh", K, q) / math.sqrt(dh), dim=1)
-            pooled = torch.einsum("blh,blhd->bhd", att, V).reshape(B, D)
+        pooled = pool_tokens(tok.float(), self.cfg, self.head32)
         h1 = F.gelu(pooled @ self.head32["head.mlp_w1"] + self.head32["head.mlp_b1"],
                     approximate="tanh")
         return h1 @ self.head32["head.mlp_w2"] + self.head32["head.mlp_b2"]
@@ -327,6 +311,29 @@ class LBVim:
 # training path (autograd through the fused kernels)
 
 
+def pool_tokens(tok, cfg: ModelConfig, head: dict):
+    """Head pooling of model.py:238-325, shared by inference and training.  Tokens
+    arrive in original order: class tokens are read at their original position
+    (the reference's p / L-1-p index map, model.py:225-229,307-312); GAP is the
+    token mean; MAP is single-query multi-head attention pooling over the tokens
+    with ``head.wk``, ``head.wv``, ``head.q`` (model.py:260-290).  Differentiable."""
+    ct = cfg.class_token
+    if ct != "none":
+        pos = {"head": [0], "middle": [cfg.num_patches // 2], "double": [0, cfg.seq_len - 1]}[ct]
+        return torch.stack([tok[:, q] for q in pos], 1).mean(1)  # graph-capturable
+    if cfg.head == "gap":
+        return tok.mean(1)
+    B, L, D = tok.shape
+    nh = cfg.map_heads
+    dh = D // nh
+    K = (tok @ head["head.wk"]).reshape(B, L, nh, dh)
+    V = (tok @ head["head.wv"]).reshape(B, L, nh, dh)
+    q = head["head.q"].reshape(nh, dh)
+    att = torch.softmax(torch.einsum("blhd,hd->blh", K, q) / math.sqrt(dh), dim=1)
+    return torch.einsum("blh,blhd->bhd", att, V).reshape(B, D)
+
+
+
 def block_forward_train(T, w: dict, M: int, reverse: bool = False, discretize_mode: str = "exp",
                         lb: bool = True, eps: float = RMS_EPS):
     """Differentiable LBVim block (block.py:158-190 forward, block.py:193-220 backward)
@@ -352,8 +359,8 @@ def block_forward_train(T, w: dict, M: int, reverse: bool = False, discretize_mo
 class LBVimTrainer:
     """LBVim training step on the fused kernels: forward with autograd, cross
     entropy, backward (lbs_scan_bwd / lbs_causal_conv1d_bwd + cuBLAS), AdamW.
-    Mirrors autodiff.train_step (autodiff.py:293-314) for the GAP / class-token
-    heads; blocks alternate direction by flip-on-load as in ``LBVim``."""
+    Mirrors autodiff.train_step (autodiff.py:293-314) for the class-token, GAP and
+    MAP heads; blocks alternate direction by flip-on-load as in ``LBVim``."""
 
     def __init__(self, cfg: ModelConfig, params: dict, lr: float = 1e-3, weight_decay: float = 0.05,
                  amp: bool = False):
@@ -386,11 +393,7 @@ class LBVimTrainer:
             w = {f: p[f"blocks.{i}.{f}"] for f in BLOCK_FIELDS}
             tok = block_forward_train(tok, w, self.M, reverse=rev and i % 2 == 1,
                                       discretize_mode=cfg.discretize_mode, lb=cfg.scan_variant == "lbm")
-        if ct != "none":
-            pos = {"head": [0], "middle": [cfg.num_patches // 2], "double": [0, cfg.seq_len - 1]}[ct]
-            pooled = torch.stack([tok[:, q] for q in pos], 1).mean(1)
-        else:
-            pooled = tok.mean(1)
+        pooled = pool_tokens(tok, cfg, p)
         h1 = F.gelu(pooled @ p["head.mlp_w1"] + p["head.mlp_b1"], approximate="tanh")
         return h1 @ p["head.mlp_w2"] + p["head.mlp_b2"]
 

@@ -257,12 +257,22 @@ def global_bidir_selective_scan(u, delta, A, B, C, D=None, z=None, delta_bias=No
     a full forward sweep with (delta, A, B, C, D, delta_bias) plus a full
     right-to-left sweep (flip-on-load) with the ``*_b`` parameters, summed, gated
     by silu(z).  Two launches of the forward-only kernel, the second accumulating
-    into the first's output; ``last_state`` is h_f + h_b like the reference."""
-    out, hf = lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8, False,
-                                     True, False)
+    into the first's output; ``last_state`` is h_f + h_b like the reference.
+    Differentiable when an input requires grad (autodiff.global_bidir_grad,
+    autodiff.py:204-236): the sum of two autograd scans, each backward one fused
+    lbs_scan_bwd launch."""
     pb = dict(delta=delta if delta_b is None else delta_b, A=A if A_b is None else A_b,
               B=B if B_b is None else B_b, C=C if C_b is None else C_b, D=D if D_b is None else D_b,
               delta_bias=delta_bias if delta_bias_b is None else delta_bias_b)
+    if _needs_grad(u, delta, A, B, C, D, z, delta_bias, *pb.values()):
+        if return_last_state:
+            raise NotImplementedError("return_last_state is not differentiable")
+        yf = lbm_selective_scan(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8, False, lb=False)
+        yb = lbm_selective_scan(u, pb["delta"], pb["A"], pb["B"], pb["C"], pb["D"], z, pb["delta_bias"],
+                                delta_softplus, 8, True, lb=False)
+        return yf + yb
+    out, hf = lbm_selective_scan_fwd(u, delta, A, B, C, D, z, delta_bias, delta_softplus, 8, False,
+                                     True, False)
     _, hb = lbm_selective_scan_fwd(u, pb["delta"], pb["A"], pb["B"], pb["C"], pb["D"], z, pb["delta_bias"],
                                    delta_softplus, 8, True, True, False, out=out, accumulate=True)
     return (out, hf + hb) if return_last_state else out

@@ -30,7 +30,9 @@ def lbm_selective_scan_op(u: torch.Tensor, delta: torch.Tensor, A: torch.Tensor,
 
 @lbm_selective_scan_op.register_fake
 def _(u, delta, A, B, C, D, z, delta_bias, delta_softplus, window, reverse):
-    return torch.empty(u.shape, dtype=u.dtype, device=u.device)
+    # the real op computes in fp32 or bf16 I/O; any other input dtype comes back fp32
+    dt = u.dtype if u.dtype in (torch.float32, torch.bfloat16) else torch.float32
+    return torch.empty(u.shape, dtype=dt, device=u.device)
 
 
 def _setup_context(ctx, inputs, output):

@@ -1,0 +1,164 @@
+"""GPU parity for launch paths the reference grid does not reach:
+
+* every window 1..16 (M in {2,5,6,7,9..15} makes the forward take its ragged-tile
+  path on every tile and the backward its multi-tile masked chunks), both
+  directions, forward and all 8 gradients;
+* long sequences whose checkpoints come from the SEQUENCE-SPLIT forward (few
+  channels: the launch plan cuts L into segments stitched by the segment
+  prefix), forced and automatic plans, forward + backward against the oracle;
+* the reference's acceptance criterion C5 (test_acceptance.py:99-142,
+  test_block.py:136-148) through the fused LBVim block: outputs before the
+  perturbed tile are BITWISE unchanged, and two blocks are dense.
+
+Oracle = oracle/lbscan_oracle.py (pinned to the unmodified reference by
+tests/test_oracle_golden.py).  Tolerances: tests/helpers.py."""
+
+import numpy as np
+import pytest
+
+from helpers import TOL_F32, TOL_GRAD, op_inputs
+from oracle import lbscan_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2506_15976_b200.scan import lbm_selective_scan_bwd, lbm_selective_scan_fwd  # noqa: E402
+
+SEQ = ("u", "delta", "z", "B", "C")
+GRADS = ("du", "ddelta", "dA", "dB", "dC", "dD", "dz", "ddelta_bias")
+
+
+def dev(x, dtype=torch.float32):
+    return None if x is None else torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+def to_dev(inp, dtype=torch.float32):
+    return {k: (dev(v, dtype) if k in SEQ else dev(v)) for k, v in inp.items()}
+
+
+def check_grads(g, ref, tol, what):
+    for k in GRADS:
+        if ref[k] is None:
+            continue
+        err = O.max_rel_err(g[k].float().cpu().numpy(), ref[k])
+        assert err <= tol, f"{what} {k}: max rel err {err:.3e} > {tol}"
+
+
+@pytest.mark.parametrize("M", [2, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15])
+@pytest.mark.parametrize("reverse", [False, True])
+@pytest.mark.parametrize("L", [37, 200])
+def test_window_grid_fwd_bwd(M, reverse, L):
+    inp = op_inputs(900 + M + L, 2, L, 40, 16)
+    t = to_dev(inp)
+    got = lbm_selective_scan_fwd(**t, window=M, reverse=reverse).cpu().numpy()
+    ref = O.lbm_selective_scan(**inp, window=M, reverse=reverse)
+    assert O.max_rel_err(got, ref) <= TOL_F32, (M, reverse, L)
+    dout = O.seeded_rng(M + L).standard_normal((2, L, 40))
+    for ck in (None, lbm_selective_scan_fwd(**t, window=M, reverse=reverse, save_checkpoints=True)[1]):
+        g = lbm_selective_scan_bwd(dev(dout), **t, window=M, reverse=reverse, checkpoints=ck)
+        rg = O.lbm_selective_scan_bwd(dout, **inp, window=M, reverse=reverse)
+        check_grads(g, rg, TOL_GRAD, f"M={M} rev={reverse} L={L} ckpt={ck is not None}")
+
+
+@pytest.mark.parametrize("M", [2, 6, 12])
+def test_window_grid_bf16(M):
+    from helpers import TOL_BF16
+    inp = op_inputs(950 + M, 2, 150, 64, 16)
+    q = {k: (v if k not in SEQ else dev(v, torch.bfloat16).float().cpu().numpy()) for k, v in inp.items()}
+    got = lbm_selective_scan_fwd(**to_dev(q, torch.bfloat16), window=M).float().cpu().numpy()
+    ref = O.lbm_selective_scan(**q, window=M)
+    assert O.max_rel_err(got, ref) <= TOL_BF16
+
+
+# ---------------------------------------------------------------------------
+# long sequences: checkpoints from the sequence-split forward, backward over
+# hundreds of chunks
+
+
+@pytest.mark.parametrize("L,E,seg", [(1024, 8, 0), (1024, 8, 5), (4096, 8, 0), (4096, 64, 0), (4096, 64, 37)])
+@pytest.mark.parametrize("reverse", [False, True])
+def test_long_sequence_split_fwd_bwd(L, E, seg, reverse):
+    """B = 1, few channels: the automatic plan (seg = 0) splits L into segments;
+    seg > 0 forces that many.  Forward output, h_final and the backward on the
+    split forward's checkpoints (and on its own recompute sweep) vs the oracle."""
+    inp = op_inputs(7000 + L + E + seg, 1, L, E, 16)
+    t = to_dev(inp)
+    out, hf, ck = lbm_selective_scan_fwd(**t, window=16, reverse=reverse, return_last_state=True,
+                                         seg_hint=seg, save_checkpoints=True)
+    ref, rhf = O.lbm_selective_scan(**inp, window=16, reverse=reverse, return_last_state=True)
+    assert O.max_rel_err(out.cpu().numpy(), ref) <= TOL_F32
+    assert O.max_rel_err(hf.cpu().numpy(), rhf) <= TOL_F32
+    dout = O.seeded_rng(L + E).standard_normal((1, L, E))
+    rg = O.lbm_selective_scan_bwd(dout, **inp, window=16, reverse=reverse)
+    g = lbm_selective_scan_bwd(dev(dout), **t, window=16, reverse=reverse, checkpoints=ck)
+    check_grads(g, rg, TOL_GRAD, f"L={L} E={E} seg={seg} rev={reverse} (split checkpoints)")
+    g2 = lbm_selective_scan_bwd(dev(dout), **t, window=16, reverse=reverse)
+    check_grads(g2, rg, TOL_GRAD, f"L={L} E={E} rev={reverse} (recompute)")
+
+
+@pytest.mark.slow
+def test_mil_bag_length_fwd_bwd_8_channels():
+    """configs[4]'s sequence length (L = 100 000, window 16) on 8 channels: the
+    forward splits L into ~780 segments; forward + backward vs the oracle."""
+    L, E = 100_000, 8
+    inp = op_inputs(7777, 1, L, E, 16)
+    t = to_dev(inp)
+    out, ck = lbm_selective_scan_fwd(**t, window=16, save_checkpoints=True)
+    ref = O.lbm_selective_scan(**inp, window=16)
+    assert O.max_rel_err(out.cpu().numpy(), ref) <= TOL_F32
+    dout = O.seeded_rng(5).standard_normal((1, L, E))
+    g = lbm_selective_scan_bwd(dev(dout), **t, window=16, checkpoints=ck)
+    rg = O.lbm_selective_scan_bwd(dout, **inp, window=16)
+    check_grads(g, rg, TOL_GRAD, "L=100k E=8")
+
+
+# ---------------------------------------------------------------------------
+# C5: receptive-field structure through the fused LBVim block
+
+
+def _c5_net(depth, seed):
+    from paper_2506_15976_b200 import model as Mdl
+    cfg = Mdl.ModelConfig(image_size=16, patch_size=4, embed_dim=8, inner_dim=12, state_dim=4, tile_len=4,
+                          num_classes=2, depth=depth)
+    return Mdl.LBVim(cfg, Mdl.init_params(cfg, seed=seed), dtype=torch.float32)
+
+
+def test_c5_receptive_field_sparsity_and_density():
+    L = 16
+    tokens = torch.tensor(O.seeded_rng(55).standard_normal((1, L, 8)), dtype=torch.float32, device="cuda")
+    net1 = _c5_net(1, 56)
+    base1 = net1.run_blocks(tokens)
+    for j in (5, 10, 15):
+        bumped = tokens.clone()
+        bumped[0, j] += 0.5
+        diff = (net1.run_blocks(bumped) != base1).any(dim=2)[0].cpu().numpy()
+        for i in range(L):
+            if j > O.tile_end(i, L, 4):
+                assert not diff[i], f"output {i} moved when token {j} (past its tile) changed"
+            else:
+                assert diff[i], f"output {i} did not see token {j}"
+    net2 = _c5_net(2, 57)
+    base2 = net2.run_blocks(tokens)
+    for j in (0, 15):
+        bumped = tokens.clone()
+        bumped[0, j] += 0.5
+        diff = (net2.run_blocks(bumped) != base2).any(dim=2)[0]
+        assert bool(diff.all()), f"2-block receptive field not dense for token {j}"
+
+
+def test_forward_only_block_is_causal():
+    """test_block.py:122-134: with M = 1 a block has zero sensitivity to the future."""
+    from paper_2506_15976_b200 import model as Mdl
+    cfg = Mdl.ModelConfig(image_size=12, patch_size=4, embed_dim=6, inner_dim=10, state_dim=4, tile_len=1,
+                          num_classes=2, depth=1)
+    net = Mdl.LBVim(cfg, Mdl.init_params(cfg, seed=13), dtype=torch.float32)
+    T = torch.tensor(O.seeded_rng(14).standard_normal((1, 9, 6)), dtype=torch.float32, device="cuda")
+    base = net.run_blocks(T)
+    for j in range(9):
+        bumped = T.clone()
+        bumped[0, j] += 0.37
+        changed = (net.run_blocks(bumped) != base).any(dim=2)[0].cpu().numpy()
+        assert not changed[:j].any(), j
+        assert changed[j]
