@@ -34,3 +34,21 @@ def test_xu_roofline_helper():
     assert r["ops_per_launch"] == 20 * 256 * 197 * 384
     assert abs(r["peak"] - 16 * 148 * 1965e6 / 1e9) < 1e-6
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12 and 0.3 < r["frac"] < 0.8
+
+
+def test_gpus_flag_self_launches_ranks():
+    """``bench.py --gpus 2`` outside torchrun starts 2 ranks itself; under the
+    reference arm rank 0 alone prints the JSON line with n_gpus = 2."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_world_size_mismatch_is_an_error():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 2
