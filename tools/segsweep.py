@@ -1,4 +1,4 @@
-"""Sequence-split sweep for the long-L configs (dev tool): seg_hint = 1, 2, 4, 8."""
+"""Sequence-split sweep (dev tool).   python tools/segsweep.py [cfg,cfg...] [S,S,...]  (S = seg_hint, 0 = auto)"""
 import json
 import os
 import sys
@@ -11,10 +11,12 @@ from kbench import CFGS, make, time_fn  # noqa: E402
 from paper_2506_15976_b200.scan import lbm_selective_scan_fwd  # noqa: E402
 
 flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-for name in ("cfg4", "cfg5", "cfg5s"):
+names = sys.argv[1].split(",") if len(sys.argv) > 1 else ["cfg4", "cfg5", "cfg5s"]
+segs = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 1, 2, 3, 4, 8, 16, 64, 256]
+for name in names:
     Bt, L, E, N, M, io, bc = CFGS[name]
     x = make(Bt, L, E, N, io, bc)
     out = torch.empty(Bt, L, E, device="cuda", dtype=io)
-    for S in (0, 1, 2, 3, 4, 8, 16, 64, 256):
+    for S in segs:
         ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, out=out, seg_hint=S), 10, flush)
         print(json.dumps(dict(cfg=name, seg_hint=S, ms=round(ms, 4))), flush=True)
