@@ -68,10 +68,21 @@ void plan_fwd(const lbs_scan_fwd_args* a, int* cta, int* n_seg, int* seg_len) {
   if (a->seg_hint > 0) {
     S = a->seg_hint;
   } else if (warps < 4 * sms && L >= 1024) {
+    // few channels, long L: the serial per-channel sweep leaves the SMs
+    // latency-bound; split L so ~8 warps per SM run (segments >= 128 steps)
     S = (8 * sms + warps - 1) / warps;
-    const int64_t max_s = L / 128;  // segments no shorter than 128 steps
+    const int64_t max_s = L / 128;
     if (S > max_s) S = max_s;
     if (S > 2048) S = 2048;
+    if (S < 1) S = 1;
+  } else if (4 * warps < sms) {
+    // short L and less than one warp per SM sub-partition (configs[0]): a few
+    // segments (each costs an aggregate pass over its steps; measured best at
+    // 8 for configs[0], 49 -> 31 us; at a few warps per SM no split pays,
+    // tools/segsweep.py)
+    S = 8;
+    const int64_t max_s = (L + 2 * m - 1) / (2 * m);  // >= 2 tiles per segment
+    if (S > max_s) S = max_s;
     if (S < 1) S = 1;
   }
   int64_t len = (L + S - 1) / S;
@@ -156,8 +167,30 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct BwdLayout {
   int64_t ckpt_len, n_ckpt;
-  size_t off_ckpt, off_seg, off_bc, off_w, total;
+  int n_seg, seg_chunks;
+  size_t off_ckpt, off_seg, off_bc, off_w, off_bagg, total;
 };
+
+// Sequence split of the backward: when the (128-channel block, batch row) CTAs
+// cannot fill one wave at 2 CTAs per SM, cut the chunk range into segments
+// (whole checkpoint chunks) so the CTAs do; the carry of the global adjoint
+// across segments comes from bwd_segment_adjoint_kernel.  Each extra segment
+// costs one light adjoint sweep over its steps; S <= kBwdMaxSeg keeps the
+// per-thread fold of the segment maps short.
+constexpr int64_t kBwdMaxSeg = 32;
+void plan_bwd(const lbs_scan_fwd_args* f, int64_t nck, int* n_seg, int* seg_chunks) {
+  const int64_t ctas = ((f->dim + lbs::kFwdThreads - 1) / lbs::kFwdThreads) * f->batch;
+  const int64_t slots = 2 * (int64_t)num_sms();
+  int64_t S = 1;
+  if (f->seg_hint > 0) S = f->seg_hint;
+  else if (ctas < slots) S = slots / ctas;
+  if (S > kBwdMaxSeg) S = kBwdMaxSeg;
+  if (S > nck) S = nck;
+  if (S < 1) S = 1;
+  const int64_t per = (nck + S - 1) / S;
+  *seg_chunks = (int)per;
+  *n_seg = (int)((nck + per - 1) / per);
+}
 
 int validate_bwd(const lbs_scan_bwd_args* a) {
   const lbs_scan_fwd_args* f = &a->fwd;
@@ -194,11 +227,14 @@ int bwd_layout(const lbs_scan_bwd_args* a, BwdLayout* lay) {
     plan_segments(&b2, &S, &len);
     if (S > 1) off += align256((size_t)f->batch * S * f->dim * 2 * NS * sizeof(float));
   }
+  plan_bwd(f, nck, &lay->n_seg, &lay->seg_chunks);
   const int64_t n_eblk = (f->dim + lbs::kFwdThreads - 1) / lbs::kFwdThreads;
   lay->off_bc = off;
   off += align256((size_t)n_eblk * f->batch * f->seqlen * 2 * NS * sizeof(float));
   lay->off_w = off;
-  off += align256((size_t)f->batch * (NS + 2) * f->dim * sizeof(float));
+  off += align256((size_t)f->batch * lay->n_seg * (NS + 2) * f->dim * sizeof(float));
+  lay->off_bagg = off;
+  if (lay->n_seg > 1) off += align256((size_t)f->batch * lay->n_seg * f->dim * 2 * NS * sizeof(float));
   lay->total = off;
   return LBS_OK;
 }
@@ -381,6 +417,9 @@ int lbs_scan_bwd(const lbs_scan_bwd_args* a, void* ws, size_t ws_bytes, void* st
   P.dz = lbs::OutView{a->dz, a->dz_stride[0], a->dz_stride[1], a->dz_stride[2]};
   P.part_bc = reinterpret_cast<float*>(w + lay.off_bc);
   P.part_w = reinterpret_cast<float*>(w + lay.off_w);
+  P.n_seg = lay.n_seg;
+  P.seg_chunks = lay.seg_chunks;
+  P.bagg = lay.n_seg > 1 ? reinterpret_cast<float*>(w + lay.off_bagg) : nullptr;
   P.dA = a->dA;
   P.dD = a->dD;
   P.dbias = a->ddelta_bias;

@@ -49,7 +49,12 @@ struct BwdParams {
   View3D dout;
   OutView du, ddelta, dz;  // io dtype; dz.p == nullptr iff no gate
   float* part_bc;          // [n_eblk][Bt][L][2][NS] dB/dC partials per channel block
-  float* part_w;           // [Bt][NS+2][E] per-row dA (NS), dD, ddelta_bias partials
+  float* part_w;           // [Bt*n_seg][NS+2][E] per-(row, segment) dA (NS), dD, ddelta_bias partials
+  // sequence split (few channels): segment s = chunks [s*seg_chunks, (s+1)*seg_chunks);
+  // bagg[(b*n_seg + s)*E + e][2*NS] = (P, M) of segment s: the carry mu = a*lam leaving
+  // the segment to the left is mu_out = P*mu_in + M (P = prod a over the segment)
+  int n_seg, seg_chunks;
+  float* bagg;
   // final outputs (reduction kernel)
   float* dA;               // (E, N)  +=
   float* dD;               // (E) or nullptr, +=

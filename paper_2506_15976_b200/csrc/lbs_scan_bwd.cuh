@@ -347,6 +347,9 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
   const bool active = e < p.E;
   const int ec = active ? e : p.E - 1;
   const int L = p.L, N = p.N, m = p.m, K = p.ckpt_len, nck = p.n_ckpt;
+  const int seg = blockIdx.z;
+  const int k_lo = seg * P.seg_chunks;
+  const int k_hi = min(nck, k_lo + P.seg_chunks);
   const bool rev = p.flags & LBS_FLAG_REVERSE;
   const bool linear = p.flags & LBS_FLAG_LINEAR;
   const bool has_z = p.z.p != nullptr;
@@ -357,7 +360,15 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
     float a1 = 2 * q + 1 < N ? p.A[(long long)ec * N + 2 * q + 1] : 0.f;
     if (!linear) { a0 *= kLog2e; a1 *= kLog2e; }
     a2s[q * kBwdThreads + tid] = mk2(a0, a1);
-    mus[q * kBwdThreads + tid] = mk2(0.f, 0.f);
+    // carry entering from the right: fold the maps of segments n_seg-1 .. seg+1
+    f2 mu = mk2(0.f, 0.f);
+    if (seg + 1 < P.n_seg) {
+      const f2* agg = reinterpret_cast<const f2*>(P.bagg) + ((long long)b * P.n_seg * p.E + ec) * NS + q;
+      const long long sstride = (long long)p.E * NS;
+#pragma unroll 8
+      for (int s = P.n_seg - 1; s > seg; --s) mu = fma2(agg[s * sstride], mu, agg[s * sstride + NP]);
+    }
+    mus[q * kBwdThreads + tid] = mu;
     dAs[q * kBwdThreads + tid] = mk2(0.f, 0.f);
   }
   BwdChunkCtx x;
@@ -397,20 +408,20 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
       cp_async8(&cks[(stg * NP + q) * kBwdThreads + tid], ckg + ((long long)k * NP + q) * p.E);
   };
 
-  int k = nck - 1;
+  int k = k_hi - 1;
   int c = k * K;
-  int clen = L - c;
+  int clen = min(K, L - c);
   stager.issue(seq, 0, c, clen);
   ck_issue(0, k);
   bcs.issue(bcraw, 0, c, clen);
   cp_async_commit();
   const int eblk = blockIdx.x;
-  for (int it = 0; k >= 0; ++it, --k) {
+  for (int it = 0; k >= k_lo; ++it, --k) {
     const int stg = it & 1;
     cp_async_wait_all();
     __syncthreads();  // chunk k landed; chunk k+1 compute (and its partial write) done
     bcs.publish(bcf, bcraw, stg, clen);
-    if (k > 0) {
+    if (k > k_lo) {
       stager.issue(seq, stg ^ 1, c - K, K);
       ck_issue(stg ^ 1, k - 1);
       bcs.issue(bcraw, stg ^ 1, c - K, K);
@@ -468,7 +479,7 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
     clen = K;
   }
   if (active) {
-    float* pw = P.part_w + (long long)b * (NS + 2) * p.E + e;
+    float* pw = P.part_w + ((long long)b * P.n_seg + seg) * (NS + 2) * p.E + e;
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       const f2 d = dAs[q * kBwdThreads + tid];
@@ -477,6 +488,116 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
     }
     pw[(long long)NS * p.E] = dD_acc;
     pw[(long long)(NS + 1) * p.E] = dbias_acc;
+  }
+}
+
+// Pass 1 of the backward's sequence split.  Segment s (steps [lo, hi)) hands
+// its left neighbour the carry mu_out = a_lo lam_lo of the global adjoint
+// lam_t = g_t + a_{t+1} lam_{t+1} (autodiff.py:125-137), g = C gy.  As a map
+// of the carry entering from the right, mu_in = a_hi lam_hi, it is affine:
+// mu_out = P mu_in + M with P = prod_{t in seg} a_t = exp(A sum dl) and M the
+// carry computed from mu_in = 0 — both per lane, computed here by one sweep
+// over the segment from the right.  (The LB record and its adjoint are
+// tile-local and segments are whole chunks of whole tiles, so nothing else
+// crosses a segment boundary; the states come from the checkpoints.)
+// p.u is the upstream gradient dout (staged in u's slot).  Segment 0's map is
+// never needed: blockIdx.z = s - 1.
+template <typename Tio, typename Tbc, int NS, bool kVec>
+__global__ void __launch_bounds__(kBwdThreads) bwd_segment_adjoint_kernel(FwdParams p, int seg_steps, float* bagg) {
+  constexpr int NP = NS / 2;
+  constexpr int CL = LBS_FWD_CL;
+  constexpr int CT = kBwdThreads;
+  using Sm = FwdSmem<Tio, Tbc, NS, CL, CT>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tio* seq = reinterpret_cast<Tio*>(smem_raw);
+  float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
+  f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
+  Tbc* bcraw = reinterpret_cast<Tbc*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes + Sm::a2_bytes);
+
+  const int tid = threadIdx.x;
+  const int e0 = blockIdx.x * CT;
+  const int e = e0 + tid;
+  const int b = blockIdx.y;
+  const int seg = blockIdx.z + 1;
+  const int n_seg = gridDim.z + 1;
+  const bool active = e < p.E;
+  const int ec = active ? e : p.E - 1;
+  const int N = p.N;
+  const bool softplus = p.flags & LBS_FLAG_SOFTPLUS;
+  const bool linear = p.flags & LBS_FLAG_LINEAR;
+  const bool has_z = p.z.p != nullptr;
+  const int lo = seg * seg_steps;
+  const int hi = min(p.L, lo + seg_steps);
+
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    float a0 = 2 * q < N ? p.A[(long long)ec * N + 2 * q] : 0.f;
+    float a1 = 2 * q + 1 < N ? p.A[(long long)ec * N + 2 * q + 1] : 0.f;
+    if (!linear) { a0 *= kLog2e; a1 *= kLog2e; }
+    a2s[q * CT + tid] = mk2(a0, a1);
+  }
+  const float bias = p.bias ? p.bias[ec] : 0.f;
+  f2 mu[NP], P[NP];
+#pragma unroll
+  for (int q = 0; q < NP; ++q) { mu[q] = mk2(0.f, 0.f); P[q] = mk2(1.f, 1.f); }
+  float dsum = 0.f;
+
+  SeqStager<Tio, kVec, CL, CT> stager;
+  stager.init(p, b, e0, has_z);
+  BcStage<Tbc, NS, CL, kVec && bc_async_ok<Tbc, NS>(), kBcIL, CT> bcs;
+  bcs.init(p, b);
+  // chunks of the segment, right to left
+  const int nch = (hi - lo + CL - 1) / CL;
+  int k = nch - 1;
+  int c = lo + k * CL;
+  int clen = hi - c;
+  stager.issue(seq, 0, c, clen);
+  bcs.issue(bcraw, 0, c, clen);
+  cp_async_commit();
+  for (int it = 0; k >= 0; ++it, --k) {
+    const int stg = it & 1;
+    cp_async_wait_all();
+    __syncthreads();
+    bcs.publish(bcf, bcraw, stg, clen);
+    if (k > 0) {
+      stager.issue(seq, stg ^ 1, c - CL, CL);
+      bcs.issue(bcraw, stg ^ 1, c - CL, CL);
+    }
+    cp_async_commit();
+    __syncthreads();
+    const Tio* sg = seq + ((size_t)stg * 3 + 0) * CL * CT;  // dout (u's slot)
+    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * CT;
+    const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * CT;
+    for (int t = clen - 1; t >= 0; --t) {
+      float dl = to_f(sd[t * CT + tid]) + bias;
+      if (softplus) dl = softplus_f(dl);
+      float gy = to_f(sg[t * CT + tid]);
+      if (has_z) gy *= silu_f(to_f(sz[t * CT + tid]));
+      dsum += dl;
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const f2 x = mul2(bc2(dl), a2s[q * CT + tid]);
+        const f2 a = linear ? x : mk2(ex2(x.x), ex2(x.y));
+        const f2 Cv = *reinterpret_cast<const f2*>(&bcf[bc_index<NS, kBcIL>(t, 1, 2 * q)]);
+        const f2 lam = fma2(bc2(gy), Cv, mu[q]);  // lam_t = g_t + a_{t+1} lam_{t+1}
+        mu[q] = mul2(a, lam);                     // carry a_t lam_t to step t-1
+        if (linear) P[q] = mul2(P[q], a);
+      }
+    }
+    c -= CL;
+    clen = CL;
+  }
+  if (!linear) {
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      const f2 x = mul2(bc2(dsum), a2s[q * CT + tid]);
+      P[q] = mk2(ex2(x.x), ex2(x.y));
+    }
+  }
+  if (active) {
+    f2* out = reinterpret_cast<f2*>(bagg + ((((long long)b * n_seg + seg) * p.E + e) * (2 * NS)));
+#pragma unroll
+    for (int q = 0; q < NP; ++q) { out[q] = P[q]; out[NP + q] = mu[q]; }
   }
 }
 
@@ -513,7 +634,8 @@ __global__ void bwd_reduce_w_kernel(BwdParams P) {
   const int i = idx / p.E;
   const int row = i < p.N ? i : NS + (i - p.N);
   double s = 0.0;
-  for (int b = 0; b < p.Bt; ++b) s += P.part_w[((long long)b * (NS + 2) + row) * p.E + e];
+  const int rows = p.Bt * P.n_seg;  // fixed order: batch rows, segments
+  for (int r = 0; r < rows; ++r) s += P.part_w[((long long)r * (NS + 2) + row) * p.E + e];
   if (i < p.N)
     P.dA[(long long)e * p.N + i] += (float)s;
   else if (i == p.N) {
@@ -528,7 +650,15 @@ inline cudaError_t launch_bwd_t(const BwdParams& P, cudaStream_t st) {
   const size_t smem = BwdSmem<Tio, NS, KT>::total;
   const FwdParams& p = P.f;
   const int n_eblk = (p.E + kBwdThreads - 1) / kBwdThreads;
-  dim3 grid(n_eblk, p.Bt);
+  if (P.n_seg > 1) {
+    FwdParams pa = p;
+    pa.u = P.dout;  // the adjoint sweep stages dout in u's slot
+    const size_t smem1 = FwdSmem<Tio, Tbc, NS, LBS_FWD_CL, kBwdThreads>::total;
+    auto k1 = bwd_segment_adjoint_kernel<Tio, Tbc, NS, kVec>;
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    k1<<<dim3(n_eblk, p.Bt, P.n_seg - 1), kBwdThreads, smem1, st>>>(pa, P.seg_chunks * p.ckpt_len, P.bagg);
+  }
+  dim3 grid(n_eblk, p.Bt, P.n_seg);
   auto k = (p.flags & LBS_FLAG_LB) ? bwd_kernel<Tio, Tbc, NS, KT, true, kVec>
                                    : bwd_kernel<Tio, Tbc, NS, KT, false, kVec>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

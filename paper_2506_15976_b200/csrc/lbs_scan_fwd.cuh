@@ -45,6 +45,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// up to this many segments the main pass folds the segment aggregates itself
+// (a short sequential fold per thread beats a separate prefix launch)
+constexpr int kFoldMax = 32;
+
 #ifndef LBS_FWD_CL
 #define LBS_FWD_CL 16  // steps per staged chunk (raised to the tile length for long windows)
 #endif
@@ -472,10 +476,23 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
 #pragma unroll
   for (int q = 0; q < NP; ++q) h.set(q, mk2(0.f, 0.f));
   if (seg > 0) {
-    // state entering this segment: folded over the earlier segments by segment_prefix_kernel
-    const f2* PH = reinterpret_cast<const f2*>(p.seg_agg + ((((long long)b * p.n_seg + seg - 1) * p.E + ec) * (2 * NS)));
+    const f2* agg = reinterpret_cast<const f2*>(p.seg_agg) + ((long long)b * p.n_seg * p.E + ec) * NS;
+    const long long sstride = (long long)p.E * NS;  // f2 per segment
+    if (p.n_seg <= kFoldMax) {
+      // few segments: fold the raw aggregates h -> P h + H of segments 0..seg-1
+      // here (core.py:48-55 combine, left to right), no prefix kernel
 #pragma unroll
-    for (int q = 0; q < NP; ++q) h.set(q, PH[NP + q]);
+      for (int q = 0; q < NP; ++q) {
+        f2 hq = mk2(0.f, 0.f);
+#pragma unroll 8
+        for (int s = 0; s < seg; ++s) hq = fma2(agg[s * sstride + q], hq, agg[s * sstride + NP + q]);
+        h.set(q, hq);
+      }
+    } else {
+      // state entering this segment, folded by segment_prefix_kernel
+#pragma unroll
+      for (int q = 0; q < NP; ++q) h.set(q, agg[(seg - 1) * sstride + NP + q]);
+    }
   }
 
   // p.out == nullptr: checkpoint-only sweep (the backward's recompute pass)
@@ -735,8 +752,10 @@ inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     dim3 g1((p.E + CT - 1) / CT, p.Bt, p.n_seg - 1);
     k1<<<g1, block, smem1, st>>>(p);
-    const long long lanes = (long long)p.Bt * p.E * (NS / 2);  // one warp each
-    segment_prefix_kernel<NS><<<(unsigned)((lanes * 32 + 127) / 128), 128, 0, st>>>(p);
+    if (p.n_seg > kFoldMax) {
+      const long long lanes = (long long)p.Bt * p.E * (NS / 2);  // one warp each
+      segment_prefix_kernel<NS><<<(unsigned)((lanes * 32 + 127) / 128), 128, 0, st>>>(p);
+    }
   }
   dim3 grid((p.E + CT - 1) / CT, p.Bt, p.n_seg);
   // LBS_FLAG_ACCUM is instantiated for the forward-only scan (the global-bidir

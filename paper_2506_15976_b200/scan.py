@@ -173,7 +173,7 @@ def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
 
 def lbm_selective_scan_bwd(dout, u, delta, A, B, C, D=None, z=None, delta_bias=None,
                            delta_softplus=True, window=None, reverse=False, lb=True,
-                           discretize_mode="exp", checkpoints=None):
+                           discretize_mode="exp", checkpoints=None, seg_hint=0):
     """Backward launch (lbs_scan_bwd): the adjoint of :func:`lbm_selective_scan_fwd`
     (autodiff.lbm_scan_grad, autodiff.py:192-195, chained through
     block._discretize_backward, block.py:106-129, and the gate).
@@ -181,7 +181,8 @@ def lbm_selective_scan_bwd(dout, u, delta, A, B, C, D=None, z=None, delta_bias=N
     Returns a dict ``du, ddelta, dz`` (io dtype, ``dz`` None without ``z``),
     ``dA`` (E, N), ``dD``, ``ddelta_bias`` (E,) and ``dB``, ``dC`` (B, L, N), all
     fp32.  ``checkpoints`` is the buffer from ``save_checkpoints=True`` (else the
-    states are recomputed by a checkpoint-only forward sweep)."""
+    states are recomputed by a checkpoint-only forward sweep).  ``seg_hint`` > 0
+    forces that many sequence segments (testing; 0 = the launch plan's choice)."""
     u, delta, A, B, C, D, z, delta_bias, M, dims = _prepare(u, delta, A, B, C, D, z, delta_bias, window)
     Bt, L, E, N = dims
     _need_cuda("dout", dout)
@@ -191,7 +192,7 @@ def lbm_selective_scan_bwd(dout, u, delta, A, B, C, D=None, z=None, delta_bias=N
     flags = _flags(delta_softplus, reverse, lb, discretize_mode)
     dev = u.device
     a = _lib.ScanBwdArgs()
-    a.fwd = _fwd_args(u, delta, A, B, C, D, z, delta_bias, M, dims, flags, None, None)
+    a.fwd = _fwd_args(u, delta, A, B, C, D, z, delta_bias, M, dims, flags, None, None, seg_hint)
     L_ = _lib.lib()
     if checkpoints is not None:
         a.fwd.checkpoints = checkpoints.data_ptr()

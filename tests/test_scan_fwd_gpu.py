@@ -109,20 +109,26 @@ def test_window_longer_than_sequence_is_one_tile():
     assert O.max_rel_err(a, O.lbm_selective_scan(**inp, window=5)) <= TOL_F32
 
 
-def test_m1_equals_forward_bitwise_and_tile_ends():
-    """test_engine.py:98-114 on the fused kernel: LB with M=1 and LB outputs at
-    tile ends are bitwise the forward-only scan's."""
+@pytest.mark.parametrize("seg_hint", [0, 1, 3])
+def test_m1_equals_forward_bitwise_and_tile_ends(seg_hint):
+    """test_engine.py:98-114 on the fused kernel: with the same tile plan, LB with
+    M=1 and LB outputs at tile ends are bitwise the forward-only scan's (under
+    the automatic launch plan, which splits this low-parallelism shape, and
+    with forced segment counts)."""
     inp = op_inputs(21, 2, 61, 40, 16)
     t = {k: dev(v) for k, v in inp.items()}
-    fwd = selective_scan(**t).cpu().numpy()
-    m1 = lbm_selective_scan(**t, window=1).cpu().numpy()
+    fwd_for = lambda M: lbm_selective_scan_fwd(**t, window=M, lb=False, seg_hint=seg_hint).cpu().numpy()
+    fwd = fwd_for(1)
+    m1 = lbm_selective_scan_fwd(**t, window=1, seg_hint=seg_hint).cpu().numpy()
     np.testing.assert_array_equal(m1, fwd)
     for M in (3, 4, 8, 16):
-        lb = lbm_selective_scan(**t, window=M).cpu().numpy()
+        lb = lbm_selective_scan_fwd(**t, window=M, seg_hint=seg_hint).cpu().numpy()
+        fw = fwd_for(M)
         for i in range(61):
             if (i + 1) % M == 0 or i == 60:
-                np.testing.assert_array_equal(lb[:, i], fwd[:, i])
+                np.testing.assert_array_equal(lb[:, i], fw[:, i])
     assert O.max_rel_err(fwd, O.lbm_selective_scan(**inp, window=1)) <= TOL_F32
+    assert O.max_rel_err(selective_scan(**t).cpu().numpy(), O.lbm_selective_scan(**inp, window=1)) <= TOL_F32
 
 
 @pytest.mark.parametrize("S", [2, 3, 7])

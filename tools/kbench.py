@@ -63,10 +63,21 @@ def make(Bt, L, E, N, io, bc, seed=0):
                 D=torch.ones(E, device="cuda"), z=r(Bt, L, E), delta_bias=bias)
 
 
-def time_fn(fn, iters, flush):
+def time_fn(fn, iters, flush, graph=True):
+    """Median device time of fn (CUDA events, L2 flushed before each launch).  With
+    graph=True fn is captured once into a CUDA graph and replayed, so the host-side
+    wrapper cost (ctypes, allocations) cannot stretch the device timeline of the
+    small configs."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        fn = g.replay
+        fn()
+        torch.cuda.synchronize()
     ts = []
     for _ in range(iters):
         flush.zero_()
@@ -95,7 +106,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--only", default="")
-    ap.add_argument("--bwd", default="cfg1,cfg3", help="configs that also time the backward")
+    ap.add_argument("--bwd", default="cfg1,cfg3,cfg3s,cfg3b", help="configs that also time the backward")
     a = ap.parse_args()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     peak = peak_gbs()
