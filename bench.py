@@ -224,6 +224,56 @@ def cpu_reference_run(steps, warmup, batch=CPU_SAMPLE_BATCH):
                       f"reference numba engine on its verification grid)"}
 
 
+def cpu_op_baseline(reps=7):
+    """BASELINE.md §4 op-level CPU leg: the reference's fused-op composition on the
+    host (numpy discretisation block.py:90-98 + the engine restated in C/OpenMP +
+    the gate block.py:177-178, all cores), and the engine alone on pre-discretised
+    inputs (lbm_scan_par and forward_scan_par, engine.py:294-302), at the configs[0]
+    shape and on a batch sample of the configs[1] layer shape.  Median of ``reps``
+    after one warm-up (the method of cli/__init__.py:166-179); lanes/s and
+    algorithmic GB/s (SURVEY.md §8d fused-op bytes, fp32)."""
+    import numpy as np
+    from oracle import cpu_port
+    cpu_port.build()
+    threads = os.cpu_count() or 1
+    out = {}
+    for name, (Bt, L, E, N, M, scale_to) in {"cfg1": (2, 197, 192, 16, 8, 2),
+                                             "cfg2": (8, 197, 384, 16, 8, 256)}.items():
+        rng = np.random.default_rng(0)
+        f = np.float32
+        u, z = rng.standard_normal((Bt, L, E)).astype(f), rng.standard_normal((Bt, L, E)).astype(f)
+        delta = (0.5 * rng.standard_normal((Bt, L, E))).astype(f)
+        Bm, Cm = rng.standard_normal((Bt, L, N)).astype(f), rng.standard_normal((Bt, L, N)).astype(f)
+        A = -np.tile(np.arange(1, N + 1, dtype=f), (E, 1))
+        D = np.ones(E, f)
+        dt = np.exp(rng.uniform(np.log(1e-3), np.log(1e-1), E))
+        bias = (dt + np.log(-np.expm1(-dt))).astype(f)
+        dl = np.logaddexp(f(0), delta + bias)
+        abar = np.exp(dl[..., None] * A).astype(f)
+        bx = (dl[..., None] * Bm[:, :, None, :] * u[..., None]).astype(f)
+
+        def med(fn):
+            fn()
+            ts = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                fn()
+                ts.append(time.perf_counter() - t0)
+            return sorted(ts)[len(ts) // 2] * 1e3
+
+        fused = med(lambda: cpu_port.fused_op(u, delta, A, Bm, Cm, D, z, bias, M, threads=threads))
+        lbm = med(lambda: cpu_port.scan_par(abar, bx, Cm, D * u, M, True, threads=threads))
+        fwd = med(lambda: cpu_port.scan_par(abar, bx, Cm, D * u, M, False, threads=threads))
+        lanes = Bt * L * E * N
+        nb = scan_alg_bytes(Bt, L, E, N, 4, 4)
+        out[name] = {"sample": f"B={Bt} of {scale_to}, L={L}, E={E}, N={N}, M={M}, fp32",
+                     "fused_op_ms": fused, "fused_op_ms_scaled": fused * scale_to / Bt,
+                     "fused_lanes_per_s": lanes / fused * 1e3, "fused_gbs": nb / fused / 1e6,
+                     "engine_lbm_ms": lbm, "engine_fwd_ms": fwd, "engine_lbm_over_fwd": lbm / fwd,
+                     "engine_lbm_lanes_per_s": lanes / lbm * 1e3}
+    return {"cores": threads, "kind": "port", "rows": out}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
@@ -267,7 +317,9 @@ def measure_ops(peak, iters=10):
     """Kernel-level numbers for every BASELINE config on this GPU (rank 0): fused
     LB fwd, forward-only fwd (the LB/fwd cost ratio of the north star) and, for
     configs[2], the backward with training checkpoints.  CUDA events on the
-    launching stream, L2 flushed between launches, median of ``iters``."""
+    launching stream, L2 flushed between launches, median of ``iters``; the scan
+    launches are replayed from a CUDA graph so host-side wrapper time cannot stretch
+    the device timeline of the small configs."""
     import torch
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from kbench import CFGS, alg_bytes, bwd_alg_bytes, gpu_warmup, make, time_fn
@@ -290,10 +342,10 @@ def measure_ops(peak, iters=10):
         s_io = torch.tensor([], dtype=io).element_size()
         s_bc = torch.tensor([], dtype=bc).element_size()
         nb = alg_bytes(Bt, L, E, N, s_io, s_bc, s_io)
-        lb_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, out=out), iters, flush)
-        fw_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, lb=False, out=out), iters, flush)
+        lb_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, out=out), iters, flush, graph=True)
+        fw_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, lb=False, out=out), iters, flush, graph=True)
         from paper_2506_15976_b200.scan import global_bidir_selective_scan
-        bi_ms = time_fn(lambda: global_bidir_selective_scan(**x), iters, flush) if name in ("cfg2", "cfg4") else None
+        bi_ms = time_fn(lambda: global_bidir_selective_scan(**x), iters, flush, graph=True) if name in ("cfg2", "cfg4") else None
         r = {"what": names[name], "window": M, "lbm_fwd_ms": lb_ms, "fwd_only_ms": fw_ms,
              "global_bidir_ms": bi_ms, "lb_over_bidir": (lb_ms / bi_ms) if bi_ms else None,
              "lb_over_fwd": lb_ms / fw_ms, "bytes": nb, "gbs": nb / lb_ms / 1e6, "frac": nb / lb_ms / 1e6 / peak,
@@ -302,19 +354,30 @@ def measure_ops(peak, iters=10):
             dout = torch.randn(Bt, L, E, device="cuda").to(io)
             _, ck = lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True)
             nbb = bwd_alg_bytes(Bt, L, E, N, s_io, s_bc, s_io)
-            bw_ms = time_fn(lambda: lbm_selective_scan_bwd(dout, **x, window=M, checkpoints=ck), iters, flush)
-            fck_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True), iters, flush)
+            bw_ms = time_fn(lambda: lbm_selective_scan_bwd(dout, **x, window=M, checkpoints=ck), iters, flush, graph=True)
+            fck_ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True), iters, flush, graph=True)
             r.update({"bwd_ms": bw_ms, "bwd_bytes": nbb, "bwd_gbs": nbb / bw_ms / 1e6,
                       "bwd_frac": nbb / bw_ms / 1e6 / peak, "fwd_with_ckpt_ms": fck_ms,
                       "fwd_bwd_ms": fck_ms + bw_ms, "fwd_bwd_gbs": (nb + nbb) / (fck_ms + bw_ms) / 1e6})
             del dout, ck
         res[name] = r
         del x, out
-    # configs[3] at model level: LBVim-S 1024^2 (L = 4096 + class token), batch 32, bf16 forward
+    # configs[1] model in fp32 (activations, weights, scan I/O): the precision of the
+    # reference's CPU arm, so the GPU/CPU ratio can be read like for like
     from paper_2506_15976_b200 import model as M
+    tcfg = M.lbvim_tiny()
+    net = M.LBVim(tcfg, M.init_params(tcfg, seed=0), dtype=torch.float32)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    imgs = torch.randn(256, 224, 224, 3, generator=g, device="cuda")
+    run = net.graphed(imgs)
+    ms = time_fn(run, 5, flush)
+    res["lbvim_t_fp32"] = {"what": "configs[1] LBVim-Ti forward in fp32 (fp32 scan I/O, fp32 GEMMs), batch 256",
+                           "ms_per_batch": ms, "images_per_s": 256 / ms * 1e3}
+    del net, imgs, run
+    torch.cuda.empty_cache()
+    # configs[3] at model level: LBVim-S 1024^2 (L = 4096 + class token), batch 32, bf16 forward
     cfg = M.lbvim_small(image_size=1024)
     net = M.LBVim(cfg, M.init_params(cfg, seed=0), dtype=torch.bfloat16)
-    g = torch.Generator(device="cuda").manual_seed(7)
     imgs = torch.randn(32, 1024, 1024, 3, generator=g, device="cuda").to(torch.bfloat16)
     run = net.graphed(imgs)
     ms = time_fn(run, 3, flush)
@@ -383,6 +446,85 @@ def measure_ops(peak, iters=10):
     del tr, ti, tl, flush
     torch.cuda.empty_cache()
     return res
+
+
+def strong_scaling(world, rank, dev, iters=10):
+    """Fixed-total-work rows for the BASELINE configs that shard (run on every rank,
+    device time per iteration = max over ranks of CUDA-event time on the launching
+    stream, L2 flushed outside the events):
+      * configs[2]: global batch 128 (LBVim-S scan shape, fp32) split over the ranks,
+        fused fwd with training checkpoints + fused bwd per rank, no collective;
+      * configs[4]: one bag, L=100k, E=512 split by channel (E/world per rank, B and C
+        replicated), the scan alone, then the all_gather of the (1, L, E/world) outputs
+        timed separately (SURVEY.md §8e);
+      * configs[1]: LBVim-Ti forward with a global batch of 256 split over the ranks."""
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from kbench import make
+
+    from paper_2506_15976_b200 import model as M
+    from paper_2506_15976_b200.scan import lbm_selective_scan_bwd, lbm_selective_scan_fwd
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def timed(fn, n=iters):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for _ in range(n):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e))
+        ms = sorted(ts)[len(ts) // 2]
+        t = torch.tensor([ms], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    rows = {}
+    Bl = 128 // world
+    x = make(Bl, 197, 768, 16, torch.float32, torch.float32, seed=rank)
+    dout = torch.randn(Bl, 197, 768, device=dev)
+
+    def step():
+        _, ck = lbm_selective_scan_fwd(**x, window=8, save_checkpoints=True)
+        lbm_selective_scan_bwd(dout, **x, window=8, checkpoints=ck)
+    ms = timed(step)
+    rows["cfg3_fwd_bwd"] = {"global_batch": 128, "batch_per_rank": Bl, "ms": ms,
+                            "images_per_s": 128 / ms * 1e3, "what": "fused LB scan fwd (checkpoints) + bwd, "
+                            "LBVim-S scan shape L=197 E=768 N=16 M=8 fp32"}
+    del x, dout
+    El = 512 // world
+    x = make(1, 100000, El, 16, torch.float32, torch.float32, seed=rank)
+    out = torch.empty(1, 100000, El, device=dev)
+    ms = timed(lambda: lbm_selective_scan_fwd(**x, window=16, out=out))
+    r = {"E": 512, "E_per_rank": El, "scan_ms": ms, "scan_instances_per_s": 1e5 / ms * 1e3}
+    if world > 1:
+        full = torch.empty(world, 1, 100000, El, device=dev)
+        r["all_gather_ms"] = timed(lambda: dist.all_gather_into_tensor(full, out))
+        r["all_gather_bytes_per_rank"] = out.numel() * 4 * (world - 1)
+    rows["cfg5_bag_scan"] = r
+    del x, out
+    torch.cuda.empty_cache()
+    cfg = M.lbvim_tiny()
+    Bl = 256 // world
+    net = M.LBVim(cfg, M.init_params(cfg, seed=0, device=dev), dtype=torch.bfloat16)
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    run = net.graphed(torch.randn(Bl, 224, 224, 3, generator=g, device=dev).to(torch.bfloat16))
+    ms = timed(run)
+    rows["lbvim_t_global256"] = {"global_batch": 256, "batch_per_rank": Bl, "ms": ms,
+                                 "images_per_s": 256 / ms * 1e3}
+    del net, run, flush
+    torch.cuda.empty_cache()
+    return {"note": "strong scaling: total work fixed as N grows; ms = median per iteration, max over ranks",
+            "n_gpus": world, "rows": rows}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -528,11 +670,13 @@ def run_ours(args, rank, world, local_rank):
         ops = measure_ops(peak)
     if world > 1:
         dist.barrier()
+    strong = None if args.no_strong else strong_scaling(world, rank, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference_run(steps=2, warmup=1)
+        r = cpu_reference_run(steps=10, warmup=1)
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu["op_level"] = cpu_op_baseline()
 
     if rank == 0:
         line = {
@@ -556,6 +700,7 @@ def run_ours(args, rank, world, local_rank):
                          "xu": xu_roofline(B, 197, cfg.inner_dim, cfg.state_dim, scan_ms, clk.summary())},
             "cpu_baseline": cpu,
             "ops": ops,
+            "strong_scaling": strong,
             "gpu_launches": 3 * cfg.depth * args.steps,  # rms_norm + conv1d+SiLU + fused scan per block
             "clocks": clk.summary(),
             "wall_s_timed_region": t_wall,
@@ -588,6 +733,7 @@ def main():
     ap.add_argument("--batch", type=int, default=GLOBAL_BATCH_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ops", action="store_true", help="skip the per-config kernel table")
+    ap.add_argument("--no-strong", action="store_true", help="skip the strong-scaling rows")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -63,7 +63,7 @@ def make(Bt, L, E, N, io, bc, seed=0):
                 D=torch.ones(E, device="cuda"), z=r(Bt, L, E), delta_bias=bias)
 
 
-def time_fn(fn, iters, flush, graph=True):
+def time_fn(fn, iters, flush, graph=False):
     """Median device time of fn (CUDA events, L2 flushed before each launch).  With
     graph=True fn is captured once into a CUDA graph and replayed, so the host-side
     wrapper cost (ctypes, allocations) cannot stretch the device timeline of the
@@ -120,7 +120,7 @@ def main():
         sbc = torch.tensor([], dtype=bc).element_size()
         nbytes = alg_bytes(Bt, L, E, N, s, sbc, s)
         for variant, lb in (("lbm", True), ("fwd", False)):
-            ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, lb=lb, out=out), a.iters, flush)
+            ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, lb=lb, out=out), a.iters, flush, graph=True)
             gbs = nbytes / ms / 1e6
             print(json.dumps(dict(cfg=name, variant=variant, ms=round(ms, 4), gbs=round(gbs, 1),
                                   frac=round(gbs / peak, 3), elems_per_s=Bt * L * E / ms * 1e3,
@@ -130,12 +130,12 @@ def main():
             _, ck = lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True)
             nb = bwd_alg_bytes(Bt, L, E, N, s, sbc, s)
             for variant, kw in (("bwd_ckpt", dict(checkpoints=ck)), ("bwd_recompute", {})):
-                ms = time_fn(lambda: lbm_selective_scan_bwd(dout, **x, window=M, **kw), a.iters, flush)
+                ms = time_fn(lambda: lbm_selective_scan_bwd(dout, **x, window=M, **kw), a.iters, flush, graph=True)
                 gbs = nb / ms / 1e6
                 print(json.dumps(dict(cfg=name, variant=variant, ms=round(ms, 4), gbs=round(gbs, 1),
                                       frac=round(gbs / peak, 3), lanes_per_s=Bt * L * E * N / ms * 1e3)),
                       flush=True)
-            ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True), a.iters, flush)
+            ms = time_fn(lambda: lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True), a.iters, flush, graph=True)
             print(json.dumps(dict(cfg=name, variant="lbm_fwd_with_ckpt", ms=round(ms, 4))), flush=True)
 
 

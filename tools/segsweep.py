@@ -26,5 +26,5 @@ for name in names:
             fn = lambda: lbm_selective_scan_bwd(dout, **x, window=M, checkpoints=ck, seg_hint=S)
         else:
             fn = lambda: lbm_selective_scan_fwd(**x, window=M, out=out, seg_hint=S)
-        ms = time_fn(fn, 10, flush)
+        ms = time_fn(fn, 10, flush, graph=True)
         print(json.dumps(dict(cfg=name, pass_="bwd" if bwd else "fwd", seg_hint=S, ms=round(ms, 4))), flush=True)
