@@ -58,7 +58,7 @@ def run_bench(L: int, M: int, workers: int, reps: int, ben: int = 1 << 16, seed:
     import torch
 
     from . import engine
-    from .scan import lbm_selective_scan_fwd
+    from .scan import global_bidir_selective_scan, lbm_selective_scan_fwd
     from .tiling import TilePlan
 
     if min(L, M, reps) < 1:
@@ -88,6 +88,8 @@ def run_bench(L: int, M: int, workers: int, reps: int, ben: int = 1 << 16, seed:
         out = torch.empty(1, L, E, device="cuda")
         fns["fused_forward"] = lambda: lbm_selective_scan_fwd(**x, window=M, lb=False, out=out)
         fns["fused_lbm"] = lambda: lbm_selective_scan_fwd(**x, window=M, lb=True, out=out)
+        # parameter reuse for the backward sweep, as the reference's bench does (cli/__init__.py:161-163)
+        fns["fused_global_bidir"] = lambda: global_bidir_selective_scan(**x)
     med = _device_median_ns(fns, reps)
     res = {}
     for k, ns in med.items():

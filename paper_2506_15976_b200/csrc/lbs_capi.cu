@@ -97,6 +97,13 @@ void plan_segments(const lbs_scan_fwd_args* a, int* n_seg, int* seg_len) {
   plan_fwd(a, &cta, n_seg, seg_len);
 }
 
+// Shapes outside the register-resident kernels (N > 16 or an effective window
+// > 16) take the state-outer generic path (lbs_generic.cu).
+bool is_generic(const lbs_scan_fwd_args* a) {
+  const int64_t m = a->window < a->seqlen ? a->window : a->seqlen;
+  return a->dstate > 16 || m > 16;
+}
+
 int validate_fwd(const lbs_scan_fwd_args* a) {
   if (!a) return fail(LBS_ERR_INVALID, "null args");
   if (a->batch < 1 || a->seqlen < 1 || a->dim < 1 || a->dstate < 1)
@@ -117,17 +124,12 @@ int validate_fwd(const lbs_scan_fwd_args* a) {
   }
   if (!a->u || !a->delta || !a->A || !a->B || !a->C)
     return fail(LBS_ERR_INVALID, "u, delta, A, B and C must be non-null");
-  if (a->dstate > 16)
-    return fail(LBS_ERR_UNSUPPORTED, "dstate %lld > 16 is not supported by the fused kernel",
-                (long long)a->dstate);
-  {
-    const int64_t m = a->window < a->seqlen ? a->window : a->seqlen;
-    if (m > 16)
-      return fail(LBS_ERR_UNSUPPORTED, "effective window min(window, L) = %lld > 16 is not supported",
-                  (long long)m);
-  }
+  if (a->dstate > 4096) return fail(LBS_ERR_UNSUPPORTED, "dstate %lld > 4096", (long long)a->dstate);
   if ((a->flags & LBS_FLAG_ACCUM) && (a->flags & LBS_FLAG_LB))
     return fail(LBS_ERR_UNSUPPORTED, "LBS_FLAG_ACCUM is supported for the forward-only scan (no LBS_FLAG_LB)");
+  if (a->checkpoints && is_generic(a))
+    return fail(LBS_ERR_UNSUPPORTED, "training checkpoints are not used for N > 16 or windows > 16 "
+                "(the generic path recomputes; pass NULL)");
   if (a->checkpoints && a->ckpt_len != lbs_scan_ckpt_len(a->seqlen, a->window))
     return fail(LBS_ERR_INVALID, "ckpt_len %lld != lbs_scan_ckpt_len(L, window) = %lld", (long long)a->ckpt_len,
                 (long long)lbs_scan_ckpt_len(a->seqlen, a->window));
@@ -143,7 +145,6 @@ void fill_fwd_params(const lbs_scan_fwd_args* a, lbs::FwdParams* p) {
   p->N = (int)a->dstate;
   // a window longer than the sequence is one (ragged) tile (test_oracle.py:247-252)
   p->m = (int)(a->window > a->seqlen ? a->seqlen : a->window);
-  if (p->m > 16) p->m = p->L;  // unreachable after validation unless m >= L
   p->flags = a->flags;
   p->u = view(a->u, a->u_stride);
   p->delta = view(a->delta, a->delta_stride);
@@ -210,6 +211,15 @@ int bwd_layout(const lbs_scan_bwd_args* a, BwdLayout* lay) {
   const lbs_scan_fwd_args* f = &a->fwd;
   int rc = validate_fwd(f);
   if (rc != LBS_OK) return rc;
+  if (is_generic(f)) {
+    lay->ckpt_len = lay->n_ckpt = 0;
+    lay->n_seg = 1;
+    lay->seg_chunks = 0;
+    lay->off_ckpt = lay->off_seg = lay->off_bc = lay->off_w = lay->off_bagg = 0;
+    lay->total = lbs::gen_bwd_workspace_floats((int)f->batch, (int)f->seqlen, (int)f->dim, (int)f->dstate) *
+                 sizeof(float);
+    return LBS_OK;
+  }
   const int64_t K = lbs_scan_ckpt_len(f->seqlen, f->window);
   const int64_t nck = (f->seqlen + K - 1) / K;
   const int NS = padded_states(f->dstate);
@@ -263,6 +273,7 @@ int64_t lbs_select_tile_len(int64_t L) {
 
 size_t lbs_scan_fwd_workspace_bytes(const lbs_scan_fwd_args* a) {
   if (validate_fwd(a) != LBS_OK) return 0;
+  if (is_generic(a)) return lbs::gen_fwd_workspace_floats((int)a->batch, (int)a->seqlen, (int)a->dim) * sizeof(float);
   lbs_scan_fwd_args b = *a;
   if (b.window > b.seqlen) b.window = b.seqlen;
   int S, len;
@@ -280,6 +291,7 @@ int64_t lbs_scan_ckpt_len(int64_t seqlen, int64_t window) {
 
 size_t lbs_scan_ckpt_bytes(const lbs_scan_fwd_args* a) {
   if (!a || a->batch < 1 || a->seqlen < 1 || a->dim < 1 || a->dstate < 1) return 0;
+  if (is_generic(a)) return 0;  // the generic backward recomputes its states
   const int64_t K = lbs_scan_ckpt_len(a->seqlen, a->window);
   if (K < 1) return 0;
   const int64_t nck = (a->seqlen + K - 1) / K;
@@ -292,6 +304,13 @@ int lbs_scan_fwd(const lbs_scan_fwd_args* a, void* ws, size_t ws_bytes, void* st
   if (!a->out && !a->checkpoints) return fail(LBS_ERR_INVALID, "out must be non-null");
   lbs::FwdParams p{};
   fill_fwd_params(a, &p);
+  if (is_generic(a)) {
+    if (!a->out) return fail(LBS_ERR_INVALID, "out must be non-null");
+    const size_t need = lbs_scan_fwd_workspace_bytes(a);
+    if (!ws || ws_bytes < need) return fail(LBS_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    return cuda_status(lbs::launch_fwd_generic(p, static_cast<float*>(ws), a->io_dtype, a->bc_dtype, (cudaStream_t)stream),
+                       "lbs_scan_fwd (generic)");
+  }
   lbs_scan_fwd_args b = *a;
   b.window = p.m;
   plan_fwd(&b, &p.cta, &p.n_seg, &p.seg_len);
@@ -389,6 +408,26 @@ int lbs_scan_bwd(const lbs_scan_bwd_args* a, void* ws, size_t ws_bytes, void* st
   const lbs_scan_fwd_args* f = &a->fwd;
   lbs::BwdParams P{};
   fill_fwd_params(f, &P.f);
+  if (is_generic(f)) {
+    P.dout = view(a->dout, a->dout_stride);
+    P.du = lbs::OutView{a->du, a->du_stride[0], a->du_stride[1], a->du_stride[2]};
+    P.ddelta = lbs::OutView{a->ddelta, a->ddelta_stride[0], a->ddelta_stride[1], a->ddelta_stride[2]};
+    P.dz = lbs::OutView{a->dz, a->dz_stride[0], a->dz_stride[1], a->dz_stride[2]};
+    P.dA = a->dA;
+    P.dD = a->dD;
+    P.dbias = a->ddelta_bias;
+    P.dB = a->dB;
+    P.sb0 = a->dB_stride[0];
+    P.sb1 = a->dB_stride[1];
+    P.sb2 = a->dB_stride[2];
+    P.dC = a->dC;
+    P.sc0 = a->dC_stride[0];
+    P.sc1 = a->dC_stride[1];
+    P.sc2 = a->dC_stride[2];
+    P.part_w = reinterpret_cast<float*>(w) + 7 * (size_t)f->batch * f->seqlen * f->dim;
+    return cuda_status(lbs::launch_bwd_generic(P, reinterpret_cast<float*>(w), f->io_dtype, f->bc_dtype, st),
+                       "lbs_scan_bwd (generic)");
+  }
   P.f.out = nullptr;
   P.f.last_state = nullptr;
   P.f.n_seg = 1;

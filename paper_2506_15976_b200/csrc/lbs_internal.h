@@ -68,6 +68,13 @@ struct BwdParams {
 cudaError_t launch_bwd(const BwdParams& p, int io_dtype, int bc_dtype, cudaStream_t st);
 int bwd_chunk_len(int m);  // steps per backward chunk (= checkpoint spacing) for window m
 
+// Generic fused path (lbs_generic.cu): windows min(M, L) > 16 or N > 16.
+size_t gen_fwd_workspace_floats(int Bt, int L, int E);
+size_t gen_bwd_workspace_floats(int Bt, int L, int E, int N);
+cudaError_t launch_fwd_generic(const FwdParams& p, float* ws, int io_dtype, int bc_dtype, cudaStream_t st);
+// BwdParams.part_w must point at gen_bwd_workspace_floats - 7 B L E floats past ws
+cudaError_t launch_bwd_generic(const BwdParams& P, float* ws, int io_dtype, int bc_dtype, cudaStream_t st);
+
 struct PreParams {
   int Bt, L, E, N, m;
   uint32_t flags;

@@ -142,7 +142,8 @@ def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
                            out=None, seg_hint=0, save_checkpoints=False, accumulate=False):
     """Forward launch (no autograd).  Returns ``out`` or ``(out, last_state)``;
     with ``save_checkpoints`` a trailing fp32 checkpoint buffer for
-    :func:`lbm_selective_scan_bwd` is appended."""
+    :func:`lbm_selective_scan_bwd` is appended (None for shapes on the generic
+    path, N > 16 or a window > 16, whose backward recomputes the states)."""
     u, delta, A, B, C, D, z, delta_bias, M, dims = _prepare(u, delta, A, B, C, D, z, delta_bias, window)
     Bt, L, E, N = dims
     if out is None:
@@ -155,12 +156,12 @@ def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
     L_ = _lib.lib()
     ck = None
     if save_checkpoints:
+        # None for the generic path (N > 16 or a window > 16), whose backward recomputes
         nck = L_.lbs_scan_ckpt_bytes(ctypes.byref(args))
-        if nck == 0:
-            raise NotImplementedError(f"lbm_selective_scan: no checkpoint plan for L={L}, window={M}")
-        ck = torch.empty(nck // 4, dtype=torch.float32, device=u.device)
-        args.checkpoints = ck.data_ptr()
-        args.ckpt_len = L_.lbs_scan_ckpt_len(L, M)
+        if nck:
+            ck = torch.empty(nck // 4, dtype=torch.float32, device=u.device)
+            args.checkpoints = ck.data_ptr()
+            args.ckpt_len = L_.lbs_scan_ckpt_len(L, M)
     nws = L_.lbs_scan_fwd_workspace_bytes(ctypes.byref(args))
     ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=u.device) if nws else None
     rc = L_.lbs_scan_fwd(ctypes.byref(args), _ptr(ws), nws, _stream())

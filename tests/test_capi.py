@@ -81,14 +81,22 @@ def test_python_api_rejects_cpu_tensors():
         lbm_selective_scan(x, x, torch.zeros(2, 3), torch.zeros(1, 4, 3), torch.zeros(1, 4, 3))
 
 
-def test_long_window_is_rejected_not_hung():
-    """min(window, L) > 16 has no register tile: UNSUPPORTED, before any launch."""
+def test_long_window_and_many_states_take_the_generic_path():
+    """min(window, L) > 16 or N > 16 has no register tile: the state-outer generic
+    kernels run instead (any M >= 1, any N, engine.py:65-85).  They need an fp32
+    workspace of B*L*E floats (fwd), take no training checkpoints, and the argument
+    checks still run before any launch."""
     L = _lib.lib()
-    rc = L.lbs_scan_fwd(C.byref(_args(seqlen=40, window=32)), None, 0, None)
-    assert rc == _lib.LBS_ERR_UNSUPPORTED
-    assert L.lbs_scan_fwd(C.byref(_args(seqlen=40, window=64)), None, 0, None) == _lib.LBS_ERR_UNSUPPORTED
-    with pytest.raises(NotImplementedError):
-        _lib.check(rc, "lbm_selective_scan")
+    for kw in (dict(seqlen=40, window=32), dict(seqlen=40, window=64), dict(dstate=17), dict(dstate=64, window=40)):
+        a = _args(**kw)
+        need = L.lbs_scan_fwd_workspace_bytes(C.byref(a))
+        assert need == 4 * a.batch * a.seqlen * a.dim, kw
+        assert L.lbs_scan_ckpt_bytes(C.byref(a)) == 0, kw
+        rc = L.lbs_scan_fwd(C.byref(a), None, 0, None)  # no workspace: rejected, nothing launched
+        assert rc == _lib.LBS_ERR_INVALID, kw
+        with pytest.raises(ShapeError):
+            _lib.check(rc, "lbm_selective_scan")
+    assert L.lbs_scan_fwd(C.byref(_args(dstate=5000)), None, 0, None) == _lib.LBS_ERR_UNSUPPORTED
 
 
 def test_checkpoint_plan():

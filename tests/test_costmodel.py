@@ -92,5 +92,5 @@ def test_cli_bench_gpu(capsys):
     lines = capsys.readouterr().out.splitlines()
     assert lines[0] == "variant,L,M,workers,median_ns,flops,hbm_elems,tile_exchanges"
     names = [ln.split(",")[0] for ln in lines[1:] if not ln.startswith("#")]
-    assert names == ["forward", "lbm", "global_bidir", "fused_forward", "fused_lbm"]
+    assert names == ["forward", "lbm", "global_bidir", "fused_forward", "fused_lbm", "fused_global_bidir"]
     assert any(ln.startswith("# lbm/forward time ratio") for ln in lines)
