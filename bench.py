@@ -443,6 +443,13 @@ def measure_ops(peak, iters=10):
                                       "bf16-I/O fused scan / conv kernels with fp32 state, fp32 master weights + AdamW, "
                                       "batch 128",
                               "ms_per_step": ms, "images_per_s": 128 / ms * 1e3}
+    # the same step captured once into a CUDA graph (LBVimTrainer.graphed: forward,
+    # fused-kernel backward and capturable AdamW replayed as one graph launch)
+    run = tr.graphed(ti, tl)
+    ms = time_fn(lambda: run(ti, tl), 5, flush)
+    res["cfg3_train_bf16_graphed"] = {"what": "configs[2] LBVim-S bf16-autocast training step as one CUDA graph replay",
+                                      "ms_per_step": ms, "images_per_s": 128 / ms * 1e3}
+    del run
     del tr, ti, tl, flush
     torch.cuda.empty_cache()
     return res

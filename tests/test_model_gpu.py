@@ -154,3 +154,31 @@ def test_lbvim_trainer_bf16_autocast():
     tr = LBVimTrainer(cfg, init_params(cfg, seed=0), lr=3e-3, amp=True)
     losses = [tr.step(imgs, labels).item() for _ in range(8)]
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
+
+
+@pytest.mark.parametrize("amp", [False, True])
+def test_lbvim_trainer_graphed_matches_eager(amp):
+    """The CUDA-graph-captured training step (forward + fused-kernel backward +
+    capturable AdamW, one replay per step) follows the eager trainer: same losses
+    and parameters after the same steps on the same batches."""
+    from paper_2506_15976_b200.model import LBVimTrainer
+    cfg = ModelConfig(image_size=32, patch_size=4, in_channels=3, embed_dim=64, inner_dim=128, state_dim=16,
+                      depth=4, class_token="middle", num_classes=10)
+    gen = torch.Generator(device="cuda").manual_seed(2)
+    batches = [(torch.randn(16, 32, 32, 3, device="cuda", generator=gen),
+                torch.randint(0, 10, (16,), device="cuda", generator=gen)) for _ in range(6)]
+    eager = LBVimTrainer(cfg, init_params(cfg, seed=0), lr=3e-3, amp=amp)
+    graphed = LBVimTrainer(cfg, init_params(cfg, seed=0), lr=3e-3, amp=amp)
+    run = graphed.graphed(*batches[0], warmup=2)   # the 2 warm-up steps train on batches[0]
+    for _ in range(2):
+        eager.step(*batches[0])
+    # fp32: the same kernels in the same order; bf16 autocast: cuBLAS may pick other
+    # bf16 GEMM algorithms under capture, so bf16-rounding-level differences remain
+    tol = 3e-3 if amp else 1e-4
+    for x, y in batches[1:]:
+        le = eager.step(x, y).item()
+        lg = run(x, y).item()
+        assert abs(le - lg) <= tol * max(1.0, abs(le)), (le, lg)
+    for k in ("blocks.0.w_x", "blocks.3.a_log", "head.mlp_w2", "patch_w"):
+        a, b = eager.params[k].detach(), graphed.params[k].detach()
+        assert ((a - b).abs().max() / a.abs().max()).item() < tol, k
