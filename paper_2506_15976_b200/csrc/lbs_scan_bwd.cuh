@@ -603,10 +603,9 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_segment_adjoint_kernel(FwdPar
 
 // Deterministic reductions of the partials (fixed order, fp64 accumulate).
 template <int NS>
-__global__ void bwd_reduce_bc_kernel(BwdParams P, int n_eblk) {
+__device__ __forceinline__ void bwd_reduce_bc(const BwdParams& P, int n_eblk, long long idx) {
   const FwdParams& p = P.f;
   const long long total = (long long)p.Bt * p.L * 2 * p.N;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int n = idx % p.N;
   const int which = (idx / p.N) % 2;
@@ -625,16 +624,16 @@ __global__ void bwd_reduce_bc_kernel(BwdParams P, int n_eblk) {
 }
 
 template <int NS>
-__global__ void bwd_reduce_w_kernel(BwdParams P) {
+__device__ __forceinline__ void bwd_reduce_w(const BwdParams& P, int idx) {
   const FwdParams& p = P.f;
   const int total = p.E * (p.N + 2);
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int e = idx % p.E;
   const int i = idx / p.E;
   const int row = i < p.N ? i : NS + (i - p.N);
   double s = 0.0;
   const int rows = p.Bt * P.n_seg;  // fixed order: batch rows, segments
+#pragma unroll 8
   for (int r = 0; r < rows; ++r) s += P.part_w[((long long)r * (NS + 2) + row) * p.E + e];
   if (i < p.N)
     P.dA[(long long)e * p.N + i] += (float)s;
@@ -643,6 +642,16 @@ __global__ void bwd_reduce_w_kernel(BwdParams P) {
   } else if (P.dbias) {
     P.dbias[e] += (float)s;
   }
+}
+
+// both fixed-order reductions in one launch: blocks [0, nbc_blocks) reduce dB/dC over
+// the channel blocks, the rest dA/dD/dbias over the batch rows and segments
+template <int NS>
+__global__ void __launch_bounds__(256) bwd_reduce_kernel(BwdParams P, int n_eblk, int nbc_blocks) {
+  if ((int)blockIdx.x < nbc_blocks)
+    bwd_reduce_bc<NS>(P, n_eblk, (long long)blockIdx.x * blockDim.x + threadIdx.x);
+  else
+    bwd_reduce_w<NS>(P, ((int)blockIdx.x - nbc_blocks) * blockDim.x + threadIdx.x);
 }
 
 template <typename Tio, typename Tbc, int NS, int KT, bool kVec>
@@ -664,9 +673,9 @@ inline cudaError_t launch_bwd_t(const BwdParams& P, cudaStream_t st) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<grid, kBwdThreads, smem, st>>>(P);
   const long long nbc = (long long)p.Bt * p.L * 2 * p.N;
-  bwd_reduce_bc_kernel<NS><<<(unsigned)((nbc + 255) / 256), 256, 0, st>>>(P, n_eblk);
+  const int nbc_blocks = (int)((nbc + 255) / 256);
   const int nw = p.E * (p.N + 2);
-  bwd_reduce_w_kernel<NS><<<(nw + 255) / 256, 256, 0, st>>>(P);
+  bwd_reduce_kernel<NS><<<nbc_blocks + (nw + 255) / 256, 256, 0, st>>>(P, n_eblk, nbc_blocks);
   return cudaGetLastError();
 }
 
