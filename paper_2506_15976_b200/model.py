@@ -283,19 +283,42 @@ class LBVim:
 
     # -- CUDA graph ---------------------------------------------------------------
     @torch.no_grad()
-    def graphed(self, example_images):
+    def graphed(self, example_images, streams: int = 1):
         """Capture forward() for a fixed input shape; returns a callable that
-        copies new images into the static input and replays the graph."""
+        copies new images into the static input and replays the graph.
+
+        ``streams`` > 1 splits the batch into that many slices whose forwards are
+        captured on separate streams (forked from and joined to the capture
+        stream), so the graph can run one slice's latency-bound scan next to
+        another slice's tensor-core GEMMs and HBM-bound conv / RMSNorm."""
         static_in = example_images.clone()
+        B = static_in.shape[0]
+        k = max(1, min(int(streams), B))
+        cuts = [B * i // k for i in range(k + 1)]
+        side = [torch.cuda.Stream() for _ in range(k)]
+
+        def fwd_split(x):
+            if k == 1:
+                return self.forward(x)
+            main = torch.cuda.current_stream()
+            outs = []
+            for i, st in enumerate(side):
+                st.wait_stream(main)
+                with torch.cuda.stream(st):
+                    outs.append(self.forward(x[cuts[i]:cuts[i + 1]]))
+            for st in side:
+                main.wait_stream(st)
+            return torch.cat(outs, 0)
+
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(2):
-                self.forward(static_in)
+                fwd_split(static_in)
         torch.cuda.current_stream().wait_stream(s)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            static_out = self.forward(static_in)
+            static_out = fwd_split(static_in)
 
         def run(images=None):
             if images is not None:
