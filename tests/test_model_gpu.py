@@ -182,3 +182,27 @@ def test_lbvim_trainer_graphed_matches_eager(amp):
     for k in ("blocks.0.w_x", "blocks.3.a_log", "head.mlp_w2", "patch_w"):
         a, b = eager.params[k].detach(), graphed.params[k].detach()
         assert ((a - b).abs().max() / a.abs().max()).item() < tol, k
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_lbvim_tiny_full_depth_vs_oracle(dtype):
+    """The headline model at full depth (LBVim-Ti, 24 layers, 224^2, L=197) against the
+    CPU oracle on two images: fp32 at 1e-4; bf16 (the benchmarked dtype) at 5e-2 with
+    the oracle fed the same bf16-rounded weights and images (activations between
+    layers are bf16 on the GPU, fp64 in the oracle)."""
+    from paper_2506_15976_b200.model import lbvim_tiny
+    cfg = lbvim_tiny()
+    params = init_params(cfg, seed=5)
+    imgs = torch.randn(2, 224, 224, 3, device="cuda", generator=torch.Generator(device="cuda").manual_seed(6))
+    tdt = torch.float32 if dtype == "fp32" else torch.bfloat16
+    got = LBVim(cfg, params, dtype=tdt)(imgs.to(tdt)).float().cpu().numpy()
+    rnd = (lambda t: t) if dtype == "fp32" else (lambda t: t.to(torch.bfloat16))
+    npp = {k: rnd(v).double().cpu().numpy() for k, v in params.items()}
+    # the GPU model keeps A, D, delta_bias and the conv taps in fp32 (model.py: f32 casts)
+    for k in params:
+        if k.endswith(("a_log", "d_param", "delta_bias", "conv_kernel", "norm_scale")):
+            npp[k] = params[k].double().cpu().numpy()
+    ocfg = dict(image_size=224, patch_size=16, in_channels=3, embed_dim=192, inner_dim=384, state_dim=16,
+                depth=24, tile_len=None, head="gap", class_token="middle")
+    ref = O.model_forward(rnd(imgs).double().cpu().numpy(), ocfg, npp)
+    assert O.max_rel_err(got, ref) <= (1e-4 if dtype == "fp32" else 5e-2)
