@@ -54,6 +54,8 @@ enum lbs_dtype { LBS_F32 = 0, LBS_BF16 = 1, LBS_F16 = 2, LBS_F64 = 3 };
 #define LBS_FLAG_SOFTPLUS  (1u << 1) /* delta := softplus(delta + delta_bias)                  */
 #define LBS_FLAG_LB        (1u << 2) /* add the tile-local backward record (LBMamba); else fwd */
 #define LBS_FLAG_LINEAR    (1u << 3) /* discretize_mode="linear": abar = delta*A (block.py:94)  */
+#define LBS_FLAG_NO_TMA    (1u << 6) /* testing: stage the forward's inputs with cp.async rows
+                                        instead of TMA tensor copies (bitwise-equal results) */
 #define LBS_FLAG_ACCUM     (1u << 5) /* out += result (second sweep of the global-bidirectional
                                         baseline, engine.global_bidir_par, engine.py:305-327);
                                         forward-only scans (not with LBS_FLAG_LB)              */

@@ -23,6 +23,7 @@ FLAG_SOFTPLUS = 1 << 1
 FLAG_LB = 1 << 2
 FLAG_LINEAR = 1 << 3
 FLAG_ACCUM = 1 << 5
+FLAG_NO_TMA = 1 << 6  # testing: cp.async staging instead of TMA (bitwise-equal results)
 CONV_SILU = 1 << 4
 
 I64 = C.c_int64

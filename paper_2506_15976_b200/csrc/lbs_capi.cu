@@ -7,6 +7,12 @@
 #include <cstdio>
 #include <string>
 
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
+#ifndef LBS_FWD_TMA_BF16
+#define LBS_FWD_TMA_BF16 0
+#endif
+
 #include "lbs_common.cuh"
 #include "lbs_internal.h"
 
@@ -137,6 +143,58 @@ int validate_fwd(const lbs_scan_fwd_args* a) {
 }
 
 lbs::View3D view(const void* p, const int64_t* s) { return lbs::View3D{p, s[0], s[1], s[2]}; }
+
+// ---------------------------------------------------------------------------
+// TMA tensor maps for the forward's staged inputs.  The driver's encoder is
+// reached through the runtime (no libcuda link); encoding is a host-only call.
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// (inner, L, B) view with element strides s[0] (batch), s[1] (step), s[2] == 1
+bool encode_view(CUtensorMap* m, const void* base, const int64_t* s, int64_t inner, int64_t L, int64_t B,
+                 size_t es, int dtype, unsigned box_inner, unsigned box_rows) {
+  auto enc = tma_encoder();
+  if (!enc || !base || s[2] != 1) return false;
+  const uint64_t a = reinterpret_cast<uint64_t>(base);
+  const int64_t s1 = s[1] * (int64_t)es, s0 = s[0] * (int64_t)es;
+  if (a % 16 || s1 % 16 || s0 % 16 || s1 <= 0 || s0 <= 0 || s1 < inner * (int64_t)es || (B > 1 && s0 < L * s1))
+    return false;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)L, (cuuint64_t)B};
+  cuuint64_t strides[2] = {(cuuint64_t)s1, (cuuint64_t)(B > 1 ? s0 : L * s1)};
+  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t el[3] = {1, 1, 1};
+  const CUtensorMapDataType dt = dtype == LBS_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  return enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Maps for u, delta, z, B, C when every view qualifies (16-byte aligned rows of
+// whole pieces, N a full state tile of whole 16-byte rows); else false (cp.async).
+bool encode_fwd_maps(const lbs_scan_fwd_args* a, int cta, lbs::FwdTmaMaps* m) {
+  if (!lbs::fwd_tma_enabled() || (a->flags & LBS_FLAG_NO_TMA)) return false;
+  const int ns = padded_states(a->dstate);
+  const size_t es = a->io_dtype == LBS_F32 ? 4 : 2, eb = a->bc_dtype == LBS_F32 ? 4 : 2;
+  if (a->dstate != ns || (ns * eb) % 16 || (a->dim * es) % 16) return false;
+  if (a->B_stride[1] != a->C_stride[1]) return false;
+  const unsigned CL = 16;  // fwd_chunk(window <= 16)
+  return encode_view(&m->tm[0], a->u, a->u_stride, a->dim, a->seqlen, a->batch, es, a->io_dtype, cta, CL) &&
+         encode_view(&m->tm[1], a->delta, a->delta_stride, a->dim, a->seqlen, a->batch, es, a->io_dtype, cta, CL) &&
+         (!a->z || encode_view(&m->tm[2], a->z, a->z_stride, a->dim, a->seqlen, a->batch, es, a->io_dtype, cta, CL)) &&
+         encode_view(&m->tm[3], a->B, a->B_stride, ns, a->seqlen, a->batch, eb, a->bc_dtype, ns, CL) &&
+         encode_view(&m->tm[4], a->C, a->C_stride, ns, a->seqlen, a->batch, eb, a->bc_dtype, ns, CL);
+}
 
 void fill_fwd_params(const lbs_scan_fwd_args* a, lbs::FwdParams* p) {
   p->Bt = (int)a->batch;
@@ -320,6 +378,13 @@ int lbs_scan_fwd(const lbs_scan_fwd_args* a, void* ws, size_t ws_bytes, void* st
       return fail(LBS_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
     p.seg_agg = static_cast<float*>(ws);
   }
+  // TMA tensor-copy staging where it measured faster (round 2, tools/kbench.py and
+  // bench.py A/B): unsplit launches with fp32 I/O (configs[2] -1 %, its 8-GPU
+  // shard -4 %).  bf16 I/O stays on cp.async (LBVim-Ti layer +2 % with TMA), as do
+  // split launches (configs[0] +14 %).
+  lbs::FwdTmaMaps maps;
+  if (p.n_seg == 1 && (a->io_dtype == LBS_F32 || LBS_FWD_TMA_BF16) && encode_fwd_maps(a, p.cta, &maps))
+    p.tma_maps = &maps;
   return cuda_status(lbs::launch_fwd(p, a->io_dtype, a->bc_dtype, (cudaStream_t)stream), "lbs_scan_fwd");
 }
 

@@ -1,10 +1,18 @@
 // Internal (host+device) parameter blocks shared by the kernels and the C ABI layer.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace lbs {
+
+// TMA tensor maps of the forward's staged inputs (u, delta, z, B, C), each 3-D
+// (inner dim, L, B), encoded on the host per call (lbs_capi.cu) and passed to
+// the kernel as a __grid_constant__ parameter.
+struct alignas(64) FwdTmaMaps {
+  CUtensorMap tm[5];
+};
 
 constexpr int kFwdThreads = 128;  // channels per CTA
 constexpr int kFwdChunk = 64;     // steps of B/C staged in shared memory per chunk
@@ -31,7 +39,11 @@ struct FwdParams {
   // training checkpoints (state entering each ckpt chunk)
   float* ckpt;
   int ckpt_len, n_ckpt;
+  // TMA staging (host pointer, read by the launcher only; nullptr: cp.async staging)
+  const FwdTmaMaps* tma_maps;
 };
+// whether the forward's TMA staging is compiled in (LBS_FWD_TMA)
+bool fwd_tma_enabled();
 
 cudaError_t launch_fwd(const FwdParams& p, int io_dtype, int bc_dtype, cudaStream_t st);
 int fwd_padded_states(int N);  // NS used by the kernels for a given N

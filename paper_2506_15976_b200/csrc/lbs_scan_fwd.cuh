@@ -18,8 +18,11 @@
 //  * state pairs (n, n+1) use packed FFMA2/FMUL2/FADD2; exp(delta*A) is one
 //    MUFU.EX2 per state-step — the kernel is MUFU/issue-bound.
 //  * a CTA owns 128 consecutive channels of one batch row.  Chunks of CL steps
-//    of u/delta/z are staged into a 2-stage shared-memory ring with cp.async
-//    (16-byte LDGSTS, coalesced rows) one chunk ahead of the compute; B and C
+//    of u/delta/z are staged into a 2-stage shared-memory ring one chunk ahead
+//    of the compute: by TMA (one cp.async.bulk.tensor box per array per chunk
+//    from host-encoded 3-D tensor maps, issued by one thread, completing on a
+//    per-stage mbarrier, one CTA barrier per chunk) for aligned unsplit fp32
+//    launches, else by cp.async (16-byte LDGSTS, coalesced rows); B and C
 //    of the chunk (shared by all channels) are prefetched into registers one
 //    chunk ahead and published to shared memory as fp32, so the warp reads
 //    them as broadcast LDS.64.  Global-memory latency is off the critical path.
@@ -48,6 +51,47 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // up to this many segments the main pass folds the segment aggregates itself
 // (a short sequential fold per thread beats a separate prefix launch)
 constexpr int kFoldMax = 32;
+
+// ---------------------------------------------------------------------------
+// kernel parameter of the instantiations without TMA staging (no 640-byte maps)
+struct NoMaps {
+  int unused;
+};
+
+// TMA (cp.async.bulk.tensor) staging: one 3-D box copy per array per chunk,
+// issued by one thread, completing on the stage's mbarrier
+#ifndef LBS_FWD_TMA
+#define LBS_FWD_TMA 1
+#endif
+#ifndef LBS_FWD_TMA_BF16
+#define LBS_FWD_TMA_BF16 0  // TMA staging for bf16 I/O as well (measured: see lbs_capi.cu)
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "LBS_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LBS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
 
 #ifndef LBS_FWD_CL
 #define LBS_FWD_CL 16  // steps per staged chunk (raised to the tile length for long windows)
@@ -357,7 +401,9 @@ template <typename Tio, int NS, int MT, bool kLB, bool kFull, int QU, bool kRegs
 __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const Tio* sz,
                                              const float* bcf, const f2* a2s, StateStore<NS / 2, kRegs, CT>& h,
                                              int t0, int r_, float bias, bool softplus, bool linear,
-                                             const TileOut& o) {
+                                             const TileOut& o, int rs = CT) {
+  // rs: elements between the ring rows of consecutive logical steps (-CT when a
+  // TMA-staged chunk of the reverse direction holds its rows in physical order)
   constexpr int NP = NS / 2;
   const int r = kFull ? MT : r_;
   const int tid = threadIdx.x;
@@ -375,8 +421,8 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 #pragma unroll
   for (int j = 0; j < MT; ++j) {
     const bool on = kFull || j < r;
-    dl[j] = on ? to_f(sd[(t0 + j) * CT + tid]) + bias : 0.f;
-    uv[j] = on ? to_f(su[(t0 + j) * CT + tid]) : 0.f;
+    dl[j] = on ? to_f(sd[(t0 + j) * rs + tid]) + bias : 0.f;
+    uv[j] = on ? to_f(su[(t0 + j) * rs + tid]) : 0.f;
   }
   // one uniform branch per tile: the MT softplus chains (EX2 -> LG2) are
   // independent and interleave
@@ -411,7 +457,7 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
     for (int j = 0; j < MT; ++j) {
       if (j < r) {
         float y = yacc[j].x + yacc[j].y;
-        if (o.has_z) y *= silu_out<Tio>(to_f(sz[(t0 + j) * CT + tid]));
+        if (o.has_z) y *= silu_out<Tio>(to_f(sz[(t0 + j) * rs + tid]));
         if constexpr (kAccum) y += prev[j];
         st<Tio>(dst, y);
       }
@@ -430,13 +476,14 @@ constexpr int fwd_chunk(int mt) { return mt > LBS_FWD_CL ? mt : LBS_FWD_CL; }
 #define LBS_FWD_MINB16 2
 #endif
 
-template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec, bool kAccum = false, int CT = kFwdThreads>
+template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec, bool kAccum = false, int CT = kFwdThreads,
+          bool kTma = false>
 __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) * (kFwdThreads / CT))
-    fwd_kernel(FwdParams p) {
+    fwd_kernel(FwdParams p, const __grid_constant__ std::conditional_t<kTma, FwdTmaMaps, NoMaps> tmaps) {
   constexpr int NP = NS / 2;
   constexpr int CL = fwd_chunk(MT);
   using Sm = FwdSmem<Tio, Tbc, NS, CL, CT>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
   f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
@@ -501,34 +548,84 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
                                    (rev ? (long long)(L - 1) * p.so1 : 0);
   const long long ostep = rev ? -p.so1 : p.so1;
 
+  // TMA staging (aligned views, host-encoded tensor maps): thread 0 issues one box
+  // copy per array per chunk; an mbarrier per ring stage; the B/C fp32 table is
+  // double-buffered so ONE CTA barrier per chunk suffices.  Else cp.async rows.
+  static_assert(!kTma || (kVec && bc_async_ok<Tbc, NS>()), "TMA staging needs aligned rows of whole pieces");
   SeqStager<Tio, kVec, CL, CT> stager;
-  stager.init(p, b, e0, has_z);
   BcStage<Tbc, NS, CL, kVec && bc_async_ok<Tbc, NS>(), kBcIL, CT> bcs;
-  bcs.init(p, b);
+  __shared__ __align__(8) uint64_t bars[2];
+  float* bcf2 = reinterpret_cast<float*>(smem_raw + Sm::total);  // second B/C table (TMA)
+  Tbc* rawB = bcraw;                                              // TMA: [2][CL][NS] B rows
+  Tbc* rawC = bcraw + 2 * CL * NS;                                //      [2][CL][NS] C rows
+  const int narr = has_z ? 3 : 2;
+  const unsigned tma_bytes = (unsigned)(narr * CL * CT * sizeof(Tio) + 2 * CL * NS * sizeof(Tbc));
+  auto tma_issue = [&](int stg, int cc, int len) {
+    if constexpr (kTma) {
+    // logical steps [cc, cc + len): physical rows [cc, ...) forward, [L - cc - len, ...) reverse
+    const int l0 = rev ? L - cc - len : cc;
+    mbar_expect_tx(&bars[stg], tma_bytes);
+    for (int a = 0; a < narr; ++a)
+      tma_load_3d(seq + ((size_t)stg * 3 + a) * CL * CT, &tmaps.tm[a], e0, l0, b, &bars[stg]);
+    tma_load_3d(rawB + (size_t)stg * CL * NS, &tmaps.tm[3], 0, l0, b, &bars[stg]);
+    tma_load_3d(rawC + (size_t)stg * CL * NS, &tmaps.tm[4], 0, l0, b, &bars[stg]);
+    }
+  };
   // prologue: chunk 0
   int c = seg_lo;
   int clen = min(CLm, seg_hi - c);
-  stager.issue(seq, 0, c, clen);
-  bcs.issue(bcraw, 0, c, clen);
-  cp_async_commit();
+  if constexpr (kTma) {
+    if (tid == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      mbar_fence_init();
+      tma_issue(0, c, clen);
+    }
+    __syncthreads();
+  } else {
+    stager.init(p, b, e0, has_z);
+    bcs.init(p, b);
+    stager.issue(seq, 0, c, clen);
+    bcs.issue(bcraw, 0, c, clen);
+    cp_async_commit();
+  }
 
   for (int k = 0; c < seg_hi; ++k) {
     const int stg = k & 1;
     const int cn = c + clen;
     const int clen_n = cn < seg_hi ? min(CLm, seg_hi - cn) : 0;
-    cp_async_wait_all();
-    __syncthreads();  // chunk k landed (all threads); compute of chunk k-1 done
-    bcs.publish(bcf, bcraw, stg, clen);
-    if (clen_n > 0) {
-      stager.issue(seq, stg ^ 1, cn, clen_n);
-      bcs.issue(bcraw, stg ^ 1, cn, clen_n);
+    const float* bcfk = bcf;
+    int rs = CT, rb = 0;  // ring row of logical step t = rb + t * rs / CT
+    if constexpr (kTma) {
+      mbar_wait(&bars[stg], (k >> 1) & 1);
+      float* bt = stg ? bcf2 : bcf;
+      if (rev) { rs = -CT; rb = clen - 1; }
+      // B/C rows -> fp32 broadcast table in logical order
+      for (int i = tid; i < CL * 2 * NS; i += CT) {
+        const int t = i / (2 * NS), kk = i % (2 * NS);
+        const int w = kk / NS, n = kk % NS;
+        const int row = rev ? clen - 1 - t : t;
+        const Tbc* src = (w ? rawC : rawB) + ((size_t)stg * CL + row) * NS + n;
+        bt[bc_index<NS, kBcIL>(t, w, n)] = t < clen ? to_f(*src) : 0.f;
+      }
+      bcfk = bt;
+      __syncthreads();  // table visible; chunk k-1 done with ring stage stg ^ 1
+      if (tid == 0 && clen_n > 0) tma_issue(stg ^ 1, cn, clen_n);
+    } else {
+      cp_async_wait_all();
+      __syncthreads();  // chunk k landed (all threads); compute of chunk k-1 done
+      bcs.publish(bcf, bcraw, stg, clen);
+      if (clen_n > 0) {
+        stager.issue(seq, stg ^ 1, cn, clen_n);
+        bcs.issue(bcraw, stg ^ 1, cn, clen_n);
+      }
+      cp_async_commit();
+      __syncthreads();  // bcf visible
     }
-    cp_async_commit();
-    __syncthreads();  // bcf visible
 
-    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * CT;
-    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * CT;
-    const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * CT;
+    const Tio* su = seq + ((size_t)stg * 3 + 0) * CL * CT + rb * CT;
+    const Tio* sd = seq + ((size_t)stg * 3 + 1) * CL * CT + rb * CT;
+    const Tio* sz = seq + ((size_t)stg * 3 + 2) * CL * CT + rb * CT;
     const TileOut o{op, ostep, c, active && p.out != nullptr, has_z, Dv, (p.flags & LBS_FLAG_ACCUM) != 0};
     for (int t0 = 0; t0 < clen; t0 += m) {
       const int r = min(m, clen - t0);
@@ -541,7 +638,7 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
         for (int q = 0; q < NP; ++q) ck[(long long)q * p.E] = h.get(q);
       }
       if (r == MT)
-        tile_compute<Tio, NS, MT, kLB, true, QU, kRegs, kAccum, CT>(su, sd, sz, bcf, a2s, h, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, true, QU, kRegs, kAccum, CT>(su, sd, sz, bcfk, a2s, h, t0, r, bias, softplus, linear, o, rs);
       else {
         // ragged tile (at most once per segment): rolled pair loop on the smem state
         StateStore<NP, false, CT> hp;
@@ -550,7 +647,7 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
 #pragma unroll
           for (int q = 0; q < NP; ++q) hp.set(q, h.get(q));
         }
-        tile_compute<Tio, NS, MT, kLB, false, (kLB ? LBS_RAGGED_QU : 1), false, kAccum, CT>(su, sd, sz, bcf, a2s, hp, t0, r, bias, softplus, linear, o);
+        tile_compute<Tio, NS, MT, kLB, false, (kLB ? LBS_RAGGED_QU : 1), false, kAccum, CT>(su, sd, sz, bcfk, a2s, hp, t0, r, bias, softplus, linear, o, rs);
         if constexpr (kRegs) {
 #pragma unroll
           for (int q = 0; q < NP; ++q) h.set(q, hp.get(q));
@@ -580,7 +677,7 @@ __global__ void __launch_bounds__(CT) segment_state_kernel(FwdParams p) {
   constexpr int NP = NS / 2;
   constexpr int CL = LBS_FWD_CL;
   using Sm = FwdSmem<Tio, Tbc, NS, CL, CT>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
   float* bcf = reinterpret_cast<float*>(smem_raw + Sm::seq_bytes);
   f2* a2s = reinterpret_cast<f2*>(smem_raw + Sm::seq_bytes + Sm::bc_bytes);
@@ -744,7 +841,12 @@ __global__ void __launch_bounds__(128) segment_prefix_kernel(FwdParams p) {
 
 template <typename Tio, typename Tbc, int NS, int MT, bool kVec, int CT>
 inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
-  const size_t smem = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT), CT>::total;
+  using SmT = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT), CT>;
+  // TMA-staged instantiations exist for fp32 I/O only (the launch policy, lbs_capi.cu)
+  constexpr bool kTmaOk = LBS_FWD_TMA && kVec && bc_async_ok<Tbc, NS>() && (sizeof(Tio) == 4 || LBS_FWD_TMA_BF16);
+  const size_t smem = SmT::total;  // (+ the second B/C table for the TMA-staged instantiations)
+  FwdParams pk = p;
+  if (!kTmaOk) pk.tma_maps = nullptr;
   dim3 block(CT);
   if (p.n_seg > 1) {
     const size_t smem1 = FwdSmem<Tio, Tbc, NS, LBS_FWD_CL, CT>::total;
@@ -760,11 +862,22 @@ inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
   dim3 grid((p.E + CT - 1) / CT, p.Bt, p.n_seg);
   // LBS_FLAG_ACCUM is instantiated for the forward-only scan (the global-bidir
   // baseline's second sweep); the C ABI rejects ACCUM together with LB
+  if constexpr (kTmaOk) {
+    if (pk.tma_maps) {
+      auto k = (p.flags & LBS_FLAG_LB)      ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec, false, CT, true>
+               : (p.flags & LBS_FLAG_ACCUM) ? fwd_kernel<Tio, Tbc, NS, MT, false, kVec, true, CT, true>
+                                            : fwd_kernel<Tio, Tbc, NS, MT, false, kVec, false, CT, true>;
+      const size_t smem_tma = smem + SmT::bc_bytes;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tma);
+      k<<<grid, block, smem_tma, st>>>(pk, *pk.tma_maps);
+      return cudaGetLastError();
+    }
+  }
   auto k = (p.flags & LBS_FLAG_LB)      ? fwd_kernel<Tio, Tbc, NS, MT, true, kVec, false, CT>
            : (p.flags & LBS_FLAG_ACCUM) ? fwd_kernel<Tio, Tbc, NS, MT, false, kVec, true, CT>
                                         : fwd_kernel<Tio, Tbc, NS, MT, false, kVec, false, CT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k<<<grid, block, smem, st>>>(p);
+  k<<<grid, block, smem, st>>>(pk, NoMaps{0});
   return cudaGetLastError();
 }
 

@@ -139,11 +139,14 @@ def _flags(delta_softplus, reverse, lb, mode):
 def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
                            delta_softplus=True, window=None, reverse=False,
                            return_last_state=False, lb=True, discretize_mode="exp",
-                           out=None, seg_hint=0, save_checkpoints=False, accumulate=False):
+                           out=None, seg_hint=0, save_checkpoints=False, accumulate=False,
+                           tma=True):
     """Forward launch (no autograd).  Returns ``out`` or ``(out, last_state)``;
     with ``save_checkpoints`` a trailing fp32 checkpoint buffer for
     :func:`lbm_selective_scan_bwd` is appended (None for shapes on the generic
-    path, N > 16 or a window > 16, whose backward recomputes the states)."""
+    path, N > 16 or a window > 16, whose backward recomputes the states).
+    ``tma=False`` stages the inputs with cp.async rows instead of TMA tensor copies
+    (testing: the results are bitwise equal)."""
     u, delta, A, B, C, D, z, delta_bias, M, dims = _prepare(u, delta, A, B, C, D, z, delta_bias, window)
     Bt, L, E, N = dims
     if out is None:
@@ -152,6 +155,8 @@ def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
     flags = _flags(delta_softplus, reverse, lb, discretize_mode)
     if accumulate:
         flags |= _lib.FLAG_ACCUM
+    if not tma:
+        flags |= _lib.FLAG_NO_TMA
     args = _fwd_args(u, delta, A, B, C, D, z, delta_bias, M, dims, flags, out, last, seg_hint)
     L_ = _lib.lib()
     ck = None

@@ -117,3 +117,36 @@ def test_fwd_short_sequence_segments(L, S):
         ref, rhf = O.lbm_selective_scan(**inp, window=8, reverse=reverse, return_last_state=True)
         assert O.max_rel_err(y.cpu().numpy(), ref) <= TOL_F32
         assert O.max_rel_err(hf.cpu().numpy(), rhf) <= TOL_F32
+
+
+@pytest.mark.parametrize("dt", ["fp32"])  # the launch plan uses TMA staging for fp32 I/O
+@pytest.mark.parametrize("E", [384, 200, 64])
+def test_tma_staging_bitwise_equals_cp_async(dt, E):
+    """The forward's TMA tensor-copy staging (3-D maps over (E, L, B), reverse direction
+    read back from physically ordered rows, out-of-bounds columns of a partial channel
+    block zero-filled) gives bitwise the results of the cp.async staging: outputs, last
+    state and checkpoints, both directions, LB and forward-only, contiguous inputs and
+    the LBVim block's strided views (delta, B, C column slices of one projection)."""
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    g = torch.Generator(device="cuda").manual_seed(E)
+    # enough rows that the launch plan does not split the sequence (TMA staging is
+    # used for unsplit launches; seg_hint=3 below checks a split launch as well)
+    Bt, L, N = {384: 4, 200: 6, 64: 20}[E], 197, 16
+    proj = torch.randn(Bt, L, E + 2 * N + 32, generator=g, device="cuda").to(tdt)
+    xz = torch.randn(Bt, L, 2 * E, generator=g, device="cuda").to(tdt)
+    base = dict(A=-torch.rand(E, N, generator=g, device="cuda") * N - 0.5, D=torch.ones(E, device="cuda"),
+                delta_bias=torch.full((E,), -3.0, device="cuda"))
+    cases = {"views": dict(u=xz[..., :E], delta=proj[..., :E], B=proj[..., E:E + N], C=proj[..., E + N:E + 2 * N],
+                           z=xz[..., E:]),
+             "contiguous": dict(u=xz[..., :E].contiguous(), delta=proj[..., :E].contiguous(),
+                                B=proj[..., E:E + N].contiguous(), C=proj[..., E + N:E + 2 * N].contiguous(), z=None)}
+    for name, x in cases.items():
+        for reverse in (False, True):
+            for lb in (True, False):
+                for seg in (0, 3):
+                    kw = dict(window=8, reverse=reverse, lb=lb, return_last_state=True, save_checkpoints=True,
+                              seg_hint=seg)
+                    y1, h1, c1 = lbm_selective_scan_fwd(**x, **base, **kw)
+                    y0, h0, c0 = lbm_selective_scan_fwd(**x, **base, **kw, tma=False)
+                    assert torch.equal(y1, y0) and torch.equal(h1, h0) and torch.equal(c1, c0), \
+                        (name, reverse, lb, seg)
