@@ -83,3 +83,27 @@ def test_config2_backward_full_size():
     for k in ("dB", "dC"):
         assert O.max_rel_err(g[k][bsel].cpu().numpy(), reff[k]) <= TOL_GRAD, k
     assert all(torch.isfinite(v).all() for v in g.values() if v is not None)
+
+
+@pytest.mark.parametrize("name,Bt,dtype,tol", [
+    ("configs[2] shape, bf16 I/O (the amp training path)", 128, torch.bfloat16, TOL_BF16),
+    ("configs[2] 8-GPU batch shard (B=16: sequence-split backward)", 16, torch.float32, TOL_GRAD),
+])
+def test_config2_backward_variants_full_size(name, Bt, dtype, tol):
+    """The other two backward launches the benchmarks report at full size: the bf16-I/O
+    training path (fp32 state, bf16 du/ddelta/dz) and one GPU's share of the 8-way batch
+    split, whose plan cuts the sequence into segments joined by the adjoint carry."""
+    _, L, E, N, M, _ = CONFIGS["configs[2] LBVim-S layer fp32"]
+    x = make_inputs(Bt, L, E, N, dtype, seed=3)
+    dout = torch.randn(Bt, L, E, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4)).to(dtype)
+    _, ck = lbm_selective_scan_fwd(**x, window=M, save_checkpoints=True)
+    g = lbm_selective_scan_bwd(dout, **x, window=M, checkpoints=ck)
+    bsel, esel = [0, Bt - 1], [0, 7, E // 2, E - 1]
+    ref = O.lbm_selective_scan_bwd(dout[bsel][:, :, esel].double().cpu().numpy(), **subsample(x, bsel, esel), window=M)
+    for k in ("du", "ddelta", "dz"):
+        assert O.max_rel_err(g[k][bsel][:, :, esel].float().cpu().numpy(), ref[k]) <= tol, (name, k)
+    reff = O.lbm_selective_scan_bwd(dout[bsel].double().cpu().numpy(), **subsample(x, bsel, list(range(E))),
+                                    window=M)
+    for k in ("dB", "dC"):
+        assert O.max_rel_err(g[k][bsel].cpu().numpy(), reff[k]) <= tol, (name, k)
+    assert all(torch.isfinite(v).all() for v in g.values() if v is not None)
