@@ -52,3 +52,19 @@ def test_world_size_mismatch_is_an_error():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 2
+
+
+def test_cpu_op_baseline_leg():
+    """The op-level CPU leg (the reference's fused-op composition and the
+    engine alone, lanes/s and GB/s) runs on the host and reports both config rows."""
+    import bench
+
+    r = bench.cpu_op_baseline(reps=1)
+    assert r["kind"] == "port" and r["cores"] >= 1
+    for name in ("cfg1", "cfg2"):
+        row = r["rows"][name]
+        for k in ("fused_op_ms", "fused_op_ms_scaled", "fused_lanes_per_s", "fused_gbs", "engine_lbm_ms",
+                  "engine_fwd_ms", "engine_lbm_over_fwd", "sample"):
+            assert k in row, (name, k)
+        assert row["fused_op_ms"] > 0 and row["engine_lbm_ms"] > 0
+        assert row["fused_op_ms_scaled"] >= row["fused_op_ms"]
