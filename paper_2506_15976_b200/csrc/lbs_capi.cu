@@ -233,10 +233,10 @@ struct BwdLayout {
 // Sequence split of the backward: when the (128-channel block, batch row) CTAs
 // cannot fill one wave at 2 CTAs per SM, cut the chunk range into segments
 // (whole checkpoint chunks) so the CTAs do; the carry of the global adjoint
-// across segments comes from bwd_segment_adjoint_kernel.  Each extra segment
-// costs one light adjoint sweep over its steps; S <= kBwdMaxSeg keeps the
-// per-thread fold of the segment maps short.
-constexpr int64_t kBwdMaxSeg = 32;
+// across segments comes from bwd_segment_adjoint_kernel (folded inside the
+// main pass for <= 32 segments, by the parallel segment prefix beyond).  Each
+// extra segment costs one light adjoint sweep over its steps.
+constexpr int64_t kBwdMaxSeg = 2048;
 void plan_bwd(const lbs_scan_fwd_args* f, int64_t nck, int* n_seg, int* seg_chunks) {
   const int64_t ctas = ((f->dim + lbs::kFwdThreads - 1) / lbs::kFwdThreads) * f->batch;
   const int64_t slots = 2 * (int64_t)num_sms();

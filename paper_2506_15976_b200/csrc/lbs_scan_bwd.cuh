@@ -68,7 +68,11 @@ struct BwdSmem {
   // prologue (which already has e^x / computes silu(z)) for the epilogue
   static constexpr size_t sig_bytes = 2ull * KT * kBwdThreads * sizeof(float);
   static constexpr size_t off_sig = off_tr + tr_bytes;
-  static constexpr size_t total = off_sig + sig_bytes;
+  // 16-step chunks run as two 8-step halves (bwd_chunk16): the record value Q and the
+  // adjoint carry a*lam crossing from the right half to the left, per state pair
+  static constexpr size_t car_bytes = KT > 8 ? 2ull * NP * kBwdThreads * sizeof(f2) : 0;
+  static constexpr size_t off_car = off_sig + sig_bytes;
+  static constexpr size_t total = off_car + car_bytes;
 };
 
 // u / delta / z / dout rows of one chunk -> ring stage (see SeqStager).
@@ -319,6 +323,228 @@ __device__ __forceinline__ void bwd_chunk(const BwdParams& P, const BwdChunkCtx&
   }
 }
 
+// A 16-step chunk (windows 9..16: the chunk is exactly one tile, possibly the
+// ragged last one) processed as two 8-step halves, step-half outer and state pair
+// inner, so only one half's per-step accumulators (Y, Pacc, S) and per-pair
+// arrays (a, h, v) are live — the one-pass form needs both halves' and spills
+// (1.2-1.8 KB per thread).  Right half first (the adjoint runs backwards): per
+// pair an ascending pass over the left half keeps only its end values (h_7,
+// v_7, a_7), the right half's descending pass leaves the record Q_8 and the
+// carry a_8 lam_8 in shared memory, and the left half then recomputes its decays
+// (+50 % exps on 16-step windows) and finishes the tile.  Same terms and order
+// per step as bwd_chunk.
+template <typename Tio, int NS, bool kLB, bool kFull>
+__device__ __forceinline__ void bwd_chunk16(const BwdParams& P, const BwdChunkCtx& x, const Tio* su,
+                                            const Tio* sd, const Tio* sz, const Tio* sg, const float* bcf,
+                                            const f2* ck, const f2* a2s, f2* mu, f2* dAs, float* red, float* tr,
+                                            float* sig, f2* car, float& dD_acc, float& dbias_acc, Tio* dup, Tio* ddp,
+                                            Tio* dzp, long long sdu, long long sdd, long long sdz) {
+  constexpr int KT = 16, H = 8;
+  constexpr int NP = NS / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int clen = kFull ? KT : x.clen;
+  const int nL = kFull ? H : min(H, clen), nR = kFull ? H : max(0, clen - H);
+  float dl[KT], dlu[KT], gy[KT];
+  float* sig_d = sig;
+  float* sig_z = sig + KT * kBwdThreads;
+  f2* qcar = car;                        // [NP][128]: Q_8
+  f2* lcar = car + NP * kBwdThreads;     // [NP][128]: a_8 lam_8
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    const bool on = kFull || j < clen;
+    dl[j] = on ? to_f(sd[j * kBwdThreads + tid]) + x.bias : 0.f;
+    gy[j] = (on && x.active) ? to_f(sg[j * kBwdThreads + tid]) : 0.f;
+  }
+  if (x.softplus) {
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      const float xv = dl[j];
+      const float t = ex2(xv * kLog2e);
+      const float opt = 1.0f + t;
+      float sp = lg2(opt) * (1.0f / kLog2e);
+      sp = (xv > 15.0f) ? xv : sp;
+      dl[j] = (xv < -15.0f) ? t : sp;
+      const float r = rcp(opt);
+      sig_d[j * kBwdThreads + tid] = (xv > 15.0f) ? 1.0f - r : t * r;
+    }
+  }
+  if (x.has_z) {
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      if (kFull || j < clen) {
+        const float zv = to_f(sz[j * kBwdThreads + tid]);
+        const float sgm = sigmoid_f(zv);
+        sig_z[j * kBwdThreads + tid] = sgm;
+        gy[j] *= zv * sgm;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    if (!(kFull || j < clen)) dl[j] = 0.f;
+    dlu[j] = dl[j] * ((kFull || j < clen) ? to_f(su[j * kBwdThreads + tid]) : 0.f);
+  }
+
+#pragma unroll
+  for (int half = 1; half >= 0; --half) {
+    const int o = half * H;            // chunk step of the half's first step
+    const int n = half ? nR : nL;      // steps in this half
+    if (n <= 0) continue;              // uniform: the chunk is one half long
+    f2 Y[H], Pacc[H], S[H];
+#pragma unroll
+    for (int jj = 0; jj < H; ++jj) Y[jj] = Pacc[jj] = S[jj] = mk2(0.f, 0.f);
+#pragma unroll 1
+    for (int q = 0; q < NP; ++q) {
+      const f2 A2 = a2s[q * kBwdThreads + tid];
+      const f2 h0 = ck[q * kBwdThreads + tid];
+      const float* bq = bcf + 4 * q;
+      auto BC = [&](int j) -> float4 { return *reinterpret_cast<const float4*>(bq + j * 2 * NS); };
+      auto decay = [&](int j) -> f2 {
+        const f2 xa = mul2(bc2(dl[j]), A2);
+        return x.linear ? xa : mk2(ex2(xa.x), ex2(xa.y));
+      };
+      // entering the half: state, LB adjoint and decay of the step before it
+      f2 hin = h0, vin = mk2(0.f, 0.f), ain = mk2(0.f, 0.f);
+      if (half) {
+        f2 hp = h0, vv = mk2(0.f, 0.f), ap = mk2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+          const float4 bc = BC(j);
+          const f2 aj = decay(j);
+          hp = fma2(aj, hp, mul2(bc2(dlu[j]), mk2(bc.x, bc.y)));
+          if (kLB) {
+            const f2 g = mul2(bc2(gy[j]), mk2(bc.z, bc.w));
+            vv = j == 0 ? g : fma2(ap, vv, g);
+          }
+          ap = aj;
+        }
+        hin = hp;
+        vin = vv;
+        ain = ap;
+      }
+      f2 a[H], h[H], v[H];
+      f2 hp = hin;
+#pragma unroll
+      for (int jj = 0; jj < H; ++jj) {
+        const int j = o + jj;
+        if (jj < n) {
+          const float4 bc = BC(j);
+          a[jj] = decay(j);
+          hp = fma2(a[jj], hp, mul2(bc2(dlu[j]), mk2(bc.x, bc.y)));
+          h[jj] = hp;
+          if (kLB) {
+            const f2 g = mul2(bc2(gy[j]), mk2(bc.z, bc.w));
+            const f2 ap = jj > 0 ? a[jj > 0 ? jj - 1 : 0] : ain;
+            const f2 vp = jj > 0 ? v[jj > 0 ? jj - 1 : 0] : vin;
+            v[jj] = (!half && jj == 0) ? g : fma2(ap, vp, g);  // the tile starts at chunk step 0
+          }
+        } else {
+          a[jj] = h[jj] = v[jj] = mk2(0.f, 0.f);
+        }
+      }
+      // descending; the tile ends at chunk step clen - 1 (in the right half unless
+      // the chunk is at most one half long)
+      const bool end_here = half || nR == 0;
+      f2 Qn = (!half && nR > 0) ? qcar[q * kBwdThreads + tid] : mk2(0.f, 0.f);
+      const f2 lin = (!half && nR > 0) ? lcar[q * kBwdThreads + tid] : mu[q * kBwdThreads + tid];
+      f2 lam = mk2(0.f, 0.f), dAq = mk2(0.f, 0.f);
+      float* tw = tr + (size_t)warp * 32 * (KT * 4 + 4);
+#pragma unroll
+      for (int jj = H - 1; jj >= 0; --jj) {
+        const int j = o + jj;
+        f2 dBv = mk2(0.f, 0.f), dCv = mk2(0.f, 0.f);
+        if (jj < n) {
+          const float4 bc = BC(j);
+          const f2 Bv = mk2(bc.x, bc.y);
+          const f2 Cv = mk2(bc.z, bc.w);
+          const f2 bj = mul2(bc2(dlu[j]), Bv);
+          const f2 g = mul2(bc2(gy[j]), Cv);
+          const bool tend = end_here && jj == n - 1;
+          const bool tstart = !half && jj == 0;
+          f2 hr = h[jj], Qc = bj;
+          if (kLB && !tend) {
+            hr = fma2(a[jj], Qn, h[jj]);
+            Qc = fma2(a[jj], Qn, bj);
+          }
+          const f2 lamj = (jj == n - 1) ? add2(g, lin) : fma2(a[jj < H - 1 ? jj + 1 : jj], lam, g);
+          const f2 hprev = jj > 0 ? h[jj > 0 ? jj - 1 : 0] : hin;
+          f2 dab = mul2(lamj, hprev);
+          if (kLB && !tend) dab = fma2(v[jj], Qn, dab);
+          f2 dbx = lamj;
+          if (kLB && !tstart) {
+            const f2 ap = jj > 0 ? a[jj > 0 ? jj - 1 : 0] : ain;
+            const f2 vp = jj > 0 ? v[jj > 0 ? jj - 1 : 0] : vin;
+            dbx = fma2(ap, vp, dbx);
+          }
+          const f2 da = x.linear ? dab : mul2(dab, a[jj]);
+          Pacc[jj] = fma2(da, A2, Pacc[jj]);
+          dAq = fma2(da, bc2(dl[j]), dAq);
+          S[jj] = fma2(dbx, Bv, S[jj]);
+          if (x.has_z) Y[jj] = fma2(Cv, hr, Y[jj]);
+          dBv = x.active ? mul2(dbx, bc2(dlu[j])) : mk2(0.f, 0.f);
+          dCv = x.active ? mul2(hr, bc2(gy[j])) : mk2(0.f, 0.f);
+          lam = lamj;
+          Qn = Qc;
+        }
+        *reinterpret_cast<float4*>(&tw[lane * (KT * 4 + 4) + j * 4]) = make_float4(dBv.x, dBv.y, dCv.x, dCv.y);
+      }
+      // warp sums of the half's 8 steps x 4 values: lane l owns value o*4 + l
+      __syncwarp();
+      {
+        const int vv = o * 4 + lane;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 32; k += 4) {
+          s0 += tw[k * (KT * 4 + 4) + vv];
+          s1 += tw[(k + 1) * (KT * 4 + 4) + vv];
+          s2 += tw[(k + 2) * (KT * 4 + 4) + vv];
+          s3 += tw[(k + 3) * (KT * 4 + 4) + vv];
+        }
+        const int jj = vv >> 2, kind = vv & 3;
+        red[((warp * KT + jj) * 2 + (kind >> 1)) * NS + 2 * q + (kind & 1)] = (s0 + s1) + (s2 + s3);
+      }
+      __syncwarp();
+      if (half) {
+        qcar[q * kBwdThreads + tid] = Qn;               // Q_8
+        lcar[q * kBwdThreads + tid] = mul2(a[0], lam);  // a_8 lam_8
+      } else {
+        mu[q * kBwdThreads + tid] = mul2(a[0], lam);    // carry into the previous chunk
+      }
+      dAs[q * kBwdThreads + tid] = add2(dAs[q * kBwdThreads + tid], dAq);
+    }
+    // ---- per-step outputs of the half: du, ddelta, dz
+    if (x.active) {
+#pragma unroll
+      for (int jj = 0; jj < H; ++jj) {
+        const int j = o + jj;
+        if (jj < n) {
+          const float uv = to_f(su[j * kBwdThreads + tid]);
+          const float s = S[jj].x + S[jj].y;
+          const float duv = x.Dv * gy[j] + dl[j] * s;
+          const float pp = (Pacc[jj].x + Pacc[jj].y) * (x.linear ? 1.f : kLn2);
+          const float ddl = pp + uv * s;
+          const float ddv = x.softplus ? ddl * sig_d[j * kBwdThreads + tid] : ddl;
+          dbias_acc += ddv;
+          dD_acc += gy[j] * uv;
+          st<Tio>(dup + (long long)(x.c + j) * sdu, duv);
+          st<Tio>(ddp + (long long)(x.c + j) * sdd, ddv);
+          if (x.has_z) {
+            const float y = Y[jj].x + Y[jj].y + x.Dv * uv;
+            const float zv = to_f(sz[j * kBwdThreads + tid]);
+            const float sgm = sig_z[j * kBwdThreads + tid];
+            const float go = to_f(sg[j * kBwdThreads + tid]);
+            st<Tio>(dzp + (long long)(x.c + j) * sdz, go * y * sgm * (1.f + zv * (1.f - sgm)));
+          }
+        }
+      }
+    }
+  }
+}
+
+#ifndef LBS_BWD_HALVES
+#define LBS_BWD_HALVES 1
+#endif
+
 #ifndef LBS_BWD_MINB
 #define LBS_BWD_MINB 2
 #endif
@@ -365,8 +591,14 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
     if (seg + 1 < P.n_seg) {
       const f2* agg = reinterpret_cast<const f2*>(P.bagg) + ((long long)b * P.n_seg * p.E + ec) * NS + q;
       const long long sstride = (long long)p.E * NS;
+      if (P.n_seg <= kFoldMax) {
 #pragma unroll 8
-      for (int s = P.n_seg - 1; s > seg; --s) mu = fma2(agg[s * sstride], mu, agg[s * sstride + NP]);
+        for (int s = P.n_seg - 1; s > seg; --s) mu = fma2(agg[s * sstride], mu, agg[s * sstride + NP]);
+      } else {
+        // maps stored right to left and folded by segment_prefix_kernel: the H slot of
+        // reversed segment r holds the carry entering reversed segment r + 1
+        mu = agg[(long long)(P.n_seg - 2 - seg) * sstride + NP];
+      }
     }
     mus[q * kBwdThreads + tid] = mu;
     dAs[q * kBwdThreads + tid] = mk2(0.f, 0.f);
@@ -458,7 +690,16 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
 #define LBS_BWD_CHUNK(FULL, ONE)                                                                     \
   bwd_chunk<Tio, NS, KT, kLB, FULL, ONE>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, trs, sigs, dD_acc, dbias_acc, \
                                          dup, ddp, dzp, sdu, sdd, sdz)
-    if (one_tile) {
+    if constexpr (KT == 16 && LBS_BWD_HALVES) {
+      // windows 9..16: the chunk is one tile (bwd_chunk_len), run as two halves
+      f2* cars = reinterpret_cast<f2*>(smem_raw + Sm::off_car);
+      if (clen == KT)
+        bwd_chunk16<Tio, NS, kLB, true>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, trs, sigs, cars, dD_acc,
+                                        dbias_acc, dup, ddp, dzp, sdu, sdd, sdz);
+      else
+        bwd_chunk16<Tio, NS, kLB, false>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, trs, sigs, cars, dD_acc,
+                                         dbias_acc, dup, ddp, dzp, sdu, sdd, sdz);
+    } else if (one_tile) {
       if (clen == KT) LBS_BWD_CHUNK(true, true);
       else LBS_BWD_CHUNK(false, true);
     } else {
@@ -503,7 +744,8 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
 // p.u is the upstream gradient dout (staged in u's slot).  Segment 0's map is
 // never needed: blockIdx.z = s - 1.
 template <typename Tio, typename Tbc, int NS, bool kVec>
-__global__ void __launch_bounds__(kBwdThreads) bwd_segment_adjoint_kernel(FwdParams p, int seg_steps, float* bagg) {
+__global__ void __launch_bounds__(kBwdThreads) bwd_segment_adjoint_kernel(FwdParams p, int seg_steps, float* bagg,
+                                                                          bool reversed) {
   constexpr int NP = NS / 2;
   constexpr int CL = LBS_FWD_CL;
   constexpr int CT = kBwdThreads;
@@ -595,7 +837,10 @@ __global__ void __launch_bounds__(kBwdThreads) bwd_segment_adjoint_kernel(FwdPar
     }
   }
   if (active) {
-    f2* out = reinterpret_cast<f2*>(bagg + ((((long long)b * n_seg + seg) * p.E + e) * (2 * NS)));
+    // reversed: segments stored right to left, so segment_prefix_kernel's left-to-right
+    // fold yields the carry entering each segment from the right
+    const int slot = reversed ? n_seg - 1 - seg : seg;
+    f2* out = reinterpret_cast<f2*>(bagg + ((((long long)b * n_seg + slot) * p.E + e) * (2 * NS)));
 #pragma unroll
     for (int q = 0; q < NP; ++q) { out[q] = P[q]; out[NP + q] = mu[q]; }
   }
@@ -665,7 +910,15 @@ inline cudaError_t launch_bwd_t(const BwdParams& P, cudaStream_t st) {
     const size_t smem1 = FwdSmem<Tio, Tbc, NS, LBS_FWD_CL, kBwdThreads>::total;
     auto k1 = bwd_segment_adjoint_kernel<Tio, Tbc, NS, kVec>;
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-    k1<<<dim3(n_eblk, p.Bt, P.n_seg - 1), kBwdThreads, smem1, st>>>(pa, P.seg_chunks * p.ckpt_len, P.bagg);
+    const bool many = P.n_seg > kFoldMax;
+    k1<<<dim3(n_eblk, p.Bt, P.n_seg - 1), kBwdThreads, smem1, st>>>(pa, P.seg_chunks * p.ckpt_len, P.bagg, many);
+    if (many) {
+      FwdParams pp = p;
+      pp.n_seg = P.n_seg;
+      pp.seg_agg = P.bagg;
+      const long long lanes = (long long)p.Bt * p.E * (NS / 2);  // one warp each
+      segment_prefix_kernel<NS><<<(unsigned)((lanes * 32 + 127) / 128), 128, 0, st>>>(pp);
+    }
   }
   dim3 grid(n_eblk, p.Bt, P.n_seg);
   auto k = (p.flags & LBS_FLAG_LB) ? bwd_kernel<Tio, Tbc, NS, KT, true, kVec>

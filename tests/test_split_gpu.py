@@ -150,3 +150,24 @@ def test_tma_staging_bitwise_equals_cp_async(dt, E):
                     y0, h0, c0 = lbm_selective_scan_fwd(**x, **base, **kw, tma=False)
                     assert torch.equal(y1, y0) and torch.equal(h1, h0) and torch.equal(c1, c0), \
                         (name, reverse, lb, seg)
+
+
+@pytest.mark.parametrize("S", [33, 120, 250])
+def test_bwd_many_segments_prefix_path(S):
+    """More than 32 backward segments: the adjoint-carry maps are stored right to left
+    and folded by the parallel segment prefix (the long-bag training case)."""
+    inp = op_inputs(900 + S, 1, 2000, 40, 16)
+    dout = O.seeded_rng(S).standard_normal((1, 2000, 40))
+    for reverse in (False, True):
+        g = np_grads(lbm_selective_scan_bwd(dev(dout), **tens(inp), window=8, reverse=reverse, seg_hint=S))
+        ref = O.lbm_selective_scan_bwd(dout, **inp, window=8, reverse=reverse)
+        check(g, ref, TOL_GRAD, f"S={S} rev={reverse}")
+
+
+def test_bwd_long_bag_shard_auto_plan():
+    """One channel shard of the configs[4] bag shape at a reduced length (E=64, L=20k,
+    window 16): the automatic plan splits the backward into hundreds of segments."""
+    inp = op_inputs(77, 1, 20000, 64, 16)
+    dout = O.seeded_rng(78).standard_normal((1, 20000, 64))
+    g = np_grads(lbm_selective_scan_bwd(dev(dout), **tens(inp), window=16))
+    check(g, O.lbm_selective_scan_bwd(dout, **inp, window=16), TOL_GRAD, "bag shard")
