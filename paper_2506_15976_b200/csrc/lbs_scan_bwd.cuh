@@ -868,18 +868,24 @@ __device__ __forceinline__ void bwd_reduce_bc(const BwdParams& P, int n_eblk, lo
     P.dC[b * P.sc0 + tp * P.sc1 + n * P.sc2] = (float)s;
 }
 
+// one warp per output (dA[e, n], dD[e], dbias[e]): the lanes stride over the (batch
+// row, segment) partials, then a fixed xor tree — deterministic, and no long serial
+// chain when the backward was split into hundreds of segments
 template <int NS>
-__device__ __forceinline__ void bwd_reduce_w(const BwdParams& P, int idx) {
+__device__ __forceinline__ void bwd_reduce_w(const BwdParams& P, int widx) {
   const FwdParams& p = P.f;
   const int total = p.E * (p.N + 2);
-  if (idx >= total) return;
-  const int e = idx % p.E;
-  const int i = idx / p.E;
+  if (widx >= total) return;  // warp-uniform
+  const int lane = threadIdx.x & 31;
+  const int e = widx % p.E;
+  const int i = widx / p.E;
   const int row = i < p.N ? i : NS + (i - p.N);
   double s = 0.0;
-  const int rows = p.Bt * P.n_seg;  // fixed order: batch rows, segments
-#pragma unroll 8
-  for (int r = 0; r < rows; ++r) s += P.part_w[((long long)r * (NS + 2) + row) * p.E + e];
+  const int rows = p.Bt * P.n_seg;  // (batch row, segment) partials
+  for (int r = lane; r < rows; r += 32) s += P.part_w[((long long)r * (NS + 2) + row) * p.E + e];
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane != 0) return;
   if (i < p.N)
     P.dA[(long long)e * p.N + i] += (float)s;
   else if (i == p.N) {
@@ -896,7 +902,7 @@ __global__ void __launch_bounds__(256) bwd_reduce_kernel(BwdParams P, int n_eblk
   if ((int)blockIdx.x < nbc_blocks)
     bwd_reduce_bc<NS>(P, n_eblk, (long long)blockIdx.x * blockDim.x + threadIdx.x);
   else
-    bwd_reduce_w<NS>(P, ((int)blockIdx.x - nbc_blocks) * blockDim.x + threadIdx.x);
+    bwd_reduce_w<NS>(P, (((int)blockIdx.x - nbc_blocks) * blockDim.x + threadIdx.x) / 32);
 }
 
 template <typename Tio, typename Tbc, int NS, int KT, bool kVec>
@@ -927,8 +933,8 @@ inline cudaError_t launch_bwd_t(const BwdParams& P, cudaStream_t st) {
   k<<<grid, kBwdThreads, smem, st>>>(P);
   const long long nbc = (long long)p.Bt * p.L * 2 * p.N;
   const int nbc_blocks = (int)((nbc + 255) / 256);
-  const int nw = p.E * (p.N + 2);
-  bwd_reduce_kernel<NS><<<nbc_blocks + (nw + 255) / 256, 256, 0, st>>>(P, n_eblk, nbc_blocks);
+  const long long nw = (long long)p.E * (p.N + 2) * 32;  // one warp per output
+  bwd_reduce_kernel<NS><<<(unsigned)(nbc_blocks + (nw + 255) / 256), 256, 0, st>>>(P, n_eblk, nbc_blocks);
   return cudaGetLastError();
 }
 
