@@ -541,10 +541,6 @@ __device__ __forceinline__ void bwd_chunk16(const BwdParams& P, const BwdChunkCt
   }
 }
 
-#ifndef LBS_BWD_HALVES
-#define LBS_BWD_HALVES 1
-#endif
-
 #ifndef LBS_BWD_MINB
 #define LBS_BWD_MINB 2
 #endif
@@ -690,7 +686,7 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
 #define LBS_BWD_CHUNK(FULL, ONE)                                                                     \
   bwd_chunk<Tio, NS, KT, kLB, FULL, ONE>(P, x, su, sd, sz, sg, bcf, ck, a2s, mus, dAs, red, trs, sigs, dD_acc, dbias_acc, \
                                          dup, ddp, dzp, sdu, sdd, sdz)
-    if constexpr (KT == 16 && LBS_BWD_HALVES) {
+    if constexpr (KT == 16) {
       // windows 9..16: the chunk is one tile (bwd_chunk_len), run as two halves
       f2* cars = reinterpret_cast<f2*>(smem_raw + Sm::off_car);
       if (clen == KT)
