@@ -47,14 +47,19 @@ def causal_conv1d_silu_fwd(x, weight, bias=None, reverse=False, silu=True, out=N
     return out
 
 
-def causal_conv1d_silu_bwd(x, weight, bias, dout, reverse=False, silu=True):
-    """-> (dx, dweight (E,K) fp32, dbias (E,) fp32 or None)."""
+def causal_conv1d_silu_bwd(x, weight, bias, dout, reverse=False, silu=True, dx=None, dweight=None):
+    """-> (dx, dweight (E,K) fp32, dbias (E,) fp32 or None).  ``dx``: optional output
+    view (x's shape and dtype, any strides); ``dweight``: optional fp32 (E, K) buffer
+    accumulated into (+=)."""
     weight = weight.to(torch.float32).contiguous()
     bias_f = None if bias is None else bias.to(torch.float32).contiguous()
     a = _conv_args(x, weight, bias_f, reverse, silu)
     dout = dout.to(x.dtype)
-    dx = torch.empty(x.shape, dtype=x.dtype, device=x.device)
-    dw = torch.zeros(weight.shape, dtype=torch.float32, device=x.device)
+    if dx is None:
+        dx = torch.empty(x.shape, dtype=x.dtype, device=x.device)
+    elif tuple(dx.shape) != tuple(x.shape) or dx.dtype != x.dtype:
+        raise ShapeError(f"dx must be a {x.dtype} tensor of shape {tuple(x.shape)}")
+    dw = torch.zeros(weight.shape, dtype=torch.float32, device=x.device) if dweight is None else dweight
     db = torch.zeros(weight.shape[0], dtype=torch.float32, device=x.device) if bias is not None else None
     a.dout, a.dout_stride = _ptr(dout), _strides(dout)
     a.dx, a.dx_stride = _ptr(dx), _strides(dx)

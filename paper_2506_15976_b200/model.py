@@ -32,6 +32,7 @@ from dataclasses import dataclass, field
 import torch
 import torch.nn.functional as F
 
+from .block_train import block_forward_fused
 from .conv import causal_conv1d_silu, causal_conv1d_silu_fwd
 from .errors import ShapeError
 from .norm import rms_norm, rms_norm_train
@@ -386,15 +387,21 @@ class LBVimTrainer:
     MAP heads; blocks alternate direction by flip-on-load as in ``LBVim``."""
 
     def __init__(self, cfg: ModelConfig, params: dict, lr: float = 1e-3, weight_decay: float = 0.05,
-                 amp: bool = False):
+                 amp: bool = False, fused_block: bool = True):
         """``amp=True``: bf16 autocast for the projections (tensor cores), so the fused
         scan / conv kernels run their bf16-I/O variants (fp32 state, fp32 master
-        weights and optimizer); default fp32 throughout, like the reference."""
+        weights and optimizer); default fp32 throughout, like the reference.
+        ``fused_block``: each block is one autograd node with a hand-written backward
+        (block_train.LBVimBlockFn: no gradient concatenations or separate residual
+        adds); False = the plain autograd composition ``block_forward_train``."""
         self.cfg = cfg
         self.amp = amp
+        self.fused_block = fused_block
         self.M = cfg.resolved_tile_len
         self.params = {k: v.detach().clone().float().requires_grad_(True) for k, v in params.items()}
-        self.opt = torch.optim.AdamW(self.params.values(), lr=lr, weight_decay=weight_decay)
+        # one fused multi-tensor AdamW kernel per step on CUDA (the foreach form is ~3x the launches)
+        fused = all(p_.is_cuda for p_ in self.params.values())
+        self.opt = torch.optim.AdamW(self.params.values(), lr=lr, weight_decay=weight_decay, fused=fused)
 
     def forward(self, images):
         cfg, p = self.cfg, self.params
@@ -414,8 +421,9 @@ class LBVimTrainer:
         rev = cfg.reverse_between_blocks
         for i in range(cfg.depth):
             w = {f: p[f"blocks.{i}.{f}"] for f in BLOCK_FIELDS}
-            tok = block_forward_train(tok, w, self.M, reverse=rev and i % 2 == 1,
-                                      discretize_mode=cfg.discretize_mode, lb=cfg.scan_variant == "lbm")
+            blk = block_forward_fused if self.fused_block else block_forward_train
+            tok = blk(tok, w, self.M, reverse=rev and i % 2 == 1, discretize_mode=cfg.discretize_mode,
+                      lb=cfg.scan_variant == "lbm")
         pooled = pool_tokens(tok, cfg, p)
         h1 = F.gelu(pooled @ p["head.mlp_w1"] + p["head.mlp_b1"], approximate="tanh")
         return h1 @ p["head.mlp_w2"] + p["head.mlp_b2"]
@@ -441,7 +449,8 @@ class LBVimTrainer:
         would).  Returns ``run(images, labels) -> loss``."""
         d = self.opt.defaults
         opt = torch.optim.AdamW(self.params.values(), lr=d["lr"], betas=d["betas"], eps=d["eps"],
-                                weight_decay=d["weight_decay"], amsgrad=d["amsgrad"], capturable=True)
+                                weight_decay=d["weight_decay"], amsgrad=d["amsgrad"], capturable=True,
+                                fused=bool(d.get("fused")))
         for p_, st in self.opt.state.items():
             opt.state[p_] = {k: (v.to(p_.device) if torch.is_tensor(v) else torch.tensor(float(v), device=p_.device))
                              for k, v in st.items()}

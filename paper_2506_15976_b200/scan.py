@@ -179,7 +179,7 @@ def lbm_selective_scan_fwd(u, delta, A, B, C, D=None, z=None, delta_bias=None,
 
 def lbm_selective_scan_bwd(dout, u, delta, A, B, C, D=None, z=None, delta_bias=None,
                            delta_softplus=True, window=None, reverse=False, lb=True,
-                           discretize_mode="exp", checkpoints=None, seg_hint=0):
+                           discretize_mode="exp", checkpoints=None, seg_hint=0, grads=None):
     """Backward launch (lbs_scan_bwd): the adjoint of :func:`lbm_selective_scan_fwd`
     (autodiff.lbm_scan_grad, autodiff.py:192-195, chained through
     block._discretize_backward, block.py:106-129, and the gate).
@@ -188,7 +188,10 @@ def lbm_selective_scan_bwd(dout, u, delta, A, B, C, D=None, z=None, delta_bias=N
     ``dA`` (E, N), ``dD``, ``ddelta_bias`` (E,) and ``dB``, ``dC`` (B, L, N), all
     fp32.  ``checkpoints`` is the buffer from ``save_checkpoints=True`` (else the
     states are recomputed by a checkpoint-only forward sweep).  ``seg_hint`` > 0
-    forces that many sequence segments (testing; 0 = the launch plan's choice)."""
+    forces that many sequence segments (testing; 0 = the launch plan's choice).
+    ``grads``: optional dict of preallocated outputs by the same keys (any subset; views
+    with any strides, e.g. column blocks of a fused projection's gradient); a given
+    ``dA`` / ``dD`` / ``ddelta_bias`` is accumulated into (+=), as by the C ABI."""
     u, delta, A, B, C, D, z, delta_bias, M, dims = _prepare(u, delta, A, B, C, D, z, delta_bias, window)
     Bt, L, E, N = dims
     _need_cuda("dout", dout)
@@ -203,14 +206,24 @@ def lbm_selective_scan_bwd(dout, u, delta, A, B, C, D=None, z=None, delta_bias=N
     if checkpoints is not None:
         a.fwd.checkpoints = checkpoints.data_ptr()
         a.fwd.ckpt_len = L_.lbs_scan_ckpt_len(L, M)
-    du = torch.empty((Bt, L, E), dtype=u.dtype, device=dev)
-    ddelta = torch.empty((Bt, L, E), dtype=u.dtype, device=dev)
-    dz = torch.empty((Bt, L, E), dtype=u.dtype, device=dev) if z is not None else None
-    dA = torch.zeros((E, N), dtype=torch.float32, device=dev)
-    dD = torch.zeros(E, dtype=torch.float32, device=dev) if D is not None else None
-    dbias = torch.zeros(E, dtype=torch.float32, device=dev) if delta_bias is not None else None
-    dB = torch.empty((Bt, L, N), dtype=torch.float32, device=dev)
-    dC = torch.empty((Bt, L, N), dtype=torch.float32, device=dev)
+    g = grads or {}
+
+    def out(key, shape, dtype, make):
+        t = g.get(key)
+        if t is None:
+            return make(shape, dtype=dtype, device=dev)
+        if tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_cuda:
+            raise ShapeError(f"grads[{key!r}] must be a CUDA {dtype} tensor of shape {tuple(shape)}")
+        return t
+
+    du = out("du", (Bt, L, E), u.dtype, torch.empty)
+    ddelta = out("ddelta", (Bt, L, E), u.dtype, torch.empty)
+    dz = out("dz", (Bt, L, E), u.dtype, torch.empty) if z is not None else None
+    dA = out("dA", (E, N), torch.float32, torch.zeros)
+    dD = out("dD", (E,), torch.float32, torch.zeros) if D is not None else None
+    dbias = out("ddelta_bias", (E,), torch.float32, torch.zeros) if delta_bias is not None else None
+    dB = out("dB", (Bt, L, N), torch.float32, torch.empty)
+    dC = out("dC", (Bt, L, N), torch.float32, torch.empty)
     a.dout, a.dout_stride = _ptr(dout), _strides(dout)
     a.du, a.du_stride = _ptr(du), _strides(du)
     a.ddelta, a.ddelta_stride = _ptr(ddelta), _strides(ddelta)
