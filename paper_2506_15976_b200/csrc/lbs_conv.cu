@@ -21,6 +21,20 @@
 
 namespace lbs {
 
+#ifndef LBS_CONV_CTAS_PER_SM
+#define LBS_CONV_CTAS_PER_SM 24  // target grid size of the streaming kernel (8/12/16/24 measured: 24 best)
+#endif
+static int conv_num_sms() {
+  static int n = 0;
+  if (n <= 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 constexpr int kConvThreads = 128;
 constexpr int kConvChunk = 32;
 constexpr int kMaxWidth = 8;
@@ -168,95 +182,6 @@ __global__ void __launch_bounds__(kConvTE) conv_fwd_tile_kernel(ConvParams p) {
     const int l = l0 + j;
     *reinterpret_cast<uint4*>(ob + (long long)(rev ? L - 1 - l : l) * p.so1 + pc * V) =
         *reinterpret_cast<const uint4*>(&yout[j][pc * V]);
-  }
-}
-
-// Two-channel variant of the tile kernel (default for whole 128-channel tiles):
-// 64 threads per (b, 32-step, 128-channel) tile, each thread sweeps a channel
-// PAIR -- one 4-byte (bf16) / 8-byte (fp32) shared-memory access, packed FFMA2
-// taps and one F2FP per two outputs -- and the staging index math is
-// compile-time (16-byte pieces per row = 128 / V).  The single-channel kernel
-// issued ~32 instructions per output (77 % issue-active, ncu) against ~17 here.
-template <typename T, int KW>
-__global__ void __launch_bounds__(kConvTE / 2) conv_fwd_tile2_kernel(ConvParams p) {
-  constexpr int V = 16 / sizeof(T);
-  constexpr int NT = kConvTE / 2;      // threads
-  constexpr int PPR = kConvTE / V;     // 16-byte pieces per row
-  constexpr int ROWS = kConvTT + KW - 1;
-  __shared__ __align__(16) T xin[ROWS][kConvTE];
-  // output row j overwrites input row j: this thread's columns of row j were
-  // last read KW-1 steps earlier (the history lives in registers), and the
-  // vector store phase runs after the barrier -- half the shared memory, twice
-  // the resident CTAs
-  T (*yout)[kConvTE] = xin;
-  const int e0 = blockIdx.x * kConvTE;
-  const int l0 = blockIdx.y * kConvTT;
-  const int b = blockIdx.z;
-  const int L = p.L;
-  const int TT = min(kConvTT, L - l0);
-  const bool rev = p.flags & LBS_FLAG_REVERSE;
-  const bool act = p.flags & LBS_CONV_SILU;
-  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
-#pragma unroll
-  for (int i0 = 0; i0 < ROWS * PPR; i0 += NT) {
-    const int i = i0 + threadIdx.x;
-    const int r = i / PPR, pc = i % PPR;
-    const int l = l0 - (KW - 1) + r;
-    if (i < ROWS * PPR) {
-      T* dst = &xin[r][pc * V];
-      if (l >= 0 && l < L) cp_async16_conv(dst, xb + (long long)(rev ? L - 1 - l : l) * p.x.s1 + pc * V);
-      else *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-    }
-  }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
-  __syncthreads();
-  {
-    const int c = 2 * threadIdx.x;
-    const int e = e0 + c;
-    f2 w[KW];
-#pragma unroll
-    for (int q = 0; q < KW; ++q)
-      w[q] = q < p.K ? mk2(p.w[(long long)e * p.K + q], p.w[(long long)(e + 1) * p.K + q]) : mk2(0.f, 0.f);
-    const f2 bias = p.bias ? mk2(p.bias[e], p.bias[e + 1]) : mk2(0.f, 0.f);
-    auto ld2 = [&](int r) -> f2 {
-      if constexpr (sizeof(T) == 4) {
-        const float2 v = *reinterpret_cast<const float2*>(&xin[r][c]);
-        return mk2(v.x, v.y);
-      } else {
-        const unsigned u = *reinterpret_cast<const unsigned*>(&xin[r][c]);
-        return mk2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
-      }
-    };
-    f2 hist[KW];  // hist[q] = x[l - q] for the two channels
-#pragma unroll
-    for (int q = 1; q < KW; ++q) hist[q] = ld2(KW - 1 - q);
-#pragma unroll 8
-    for (int j = 0; j < kConvTT; ++j) {
-      hist[0] = ld2(KW - 1 + j);
-      f2 acc = bias;
-#pragma unroll
-      for (int q = KW - 1; q >= 0; --q) acc = fma2(w[q], hist[q], acc);
-      if (act) acc = mk2(silu_f(acc.x), silu_f(acc.y));
-      if constexpr (sizeof(T) == 4) {
-        *reinterpret_cast<float2*>(&yout[j][c]) = make_float2(acc.x, acc.y);
-      } else {
-        *reinterpret_cast<__nv_bfloat162*>(&yout[j][c]) = __floats2bfloat162_rn(acc.x, acc.y);
-      }
-#pragma unroll
-      for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
-    }
-  }
-  __syncthreads();
-  T* ob = static_cast<T*>(p.out) + (long long)b * p.so0 + e0;
-#pragma unroll
-  for (int i0 = 0; i0 < kConvTT * PPR; i0 += NT) {
-    const int i = i0 + threadIdx.x;
-    const int j = i / PPR, pc = i % PPR;
-    if (j < TT) {
-      const int l = l0 + j;
-      *reinterpret_cast<uint4*>(ob + (long long)(rev ? L - 1 - l : l) * p.so1 + pc * V) =
-          *reinterpret_cast<const uint4*>(&yout[j][pc * V]);
-    }
   }
 }
 
@@ -597,6 +522,94 @@ __global__ void __launch_bounds__(32 * kRedSlices) conv_reduce_kernel(const floa
   }
 }
 
+// Streaming forward (16-byte aligned rows, E % 128 == 0): a 64-thread CTA owns
+// 128 channels (two per thread) of one batch row over a range of `rows` logical
+// steps and streams it through a 2-stage cp.async ring of kConvST rows -- the
+// next chunk's loads are in flight while the current chunk is computed, the
+// K-1 history stays in registers across chunks (no halo reload), and each
+// thread stores its channel pair per step (a warp writes 128 contiguous bytes).
+// Replaces the one-shot tile kernel (load -> barrier -> compute -> barrier ->
+// store per 32-step tile), whose per-CTA fill and drain left the LBVim-Ti
+// layer shape at 0.46 of HBM (tools/convbench.py).
+constexpr int kConvST = 32;
+template <typename T, int KW>
+__global__ void __launch_bounds__(64) conv_fwd_stream_kernel(ConvParams p, int rows) {
+  constexpr int TE = 128, NT = 64;
+  constexpr int V = 16 / sizeof(T);
+  constexpr int PPR = TE / V;  // 16-byte pieces per row
+  __shared__ __align__(16) T ring[2][kConvST][TE];
+  const int tid = threadIdx.x;
+  const int e0 = blockIdx.x * TE;
+  const int b = blockIdx.z;
+  const int L = p.L;
+  const int lb = blockIdx.y * rows;
+  const int le = min(L, lb + rows);
+  const bool rev = p.flags & LBS_FLAG_REVERSE;
+  const bool act = p.flags & LBS_CONV_SILU;
+  const T* xb = static_cast<const T*>(p.x.p) + (long long)b * p.x.s0 + e0;
+  T* ob = static_cast<T*>(p.out) + (long long)b * p.so0 + e0;
+  auto phys = [&](int l) -> long long { return rev ? (long long)(L - 1 - l) : (long long)l; };
+  auto issue = [&](int stg, int l0) {
+#pragma unroll
+    for (int i0 = 0; i0 < kConvST * PPR; i0 += NT) {
+      const int i = i0 + tid;
+      const int r = i / PPR, pc = i % PPR;
+      if (l0 + r < le) cp_async16_conv(&ring[stg][r][pc * V], xb + phys(l0 + r) * p.x.s1 + pc * V);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if (lb >= le) return;
+  issue(0, lb);
+  const int c = 2 * tid;
+  const int e = e0 + c;
+  f2 w[KW];
+#pragma unroll
+  for (int q = 0; q < KW; ++q)
+    w[q] = q < p.K ? mk2(p.w[(long long)e * p.K + q], p.w[(long long)(e + 1) * p.K + q]) : mk2(0.f, 0.f);
+  const f2 bias = p.bias ? mk2(p.bias[e], p.bias[e + 1]) : mk2(0.f, 0.f);
+  f2 hist[KW];  // hist[q] = x[l - q] for the two channels
+  hist[0] = mk2(0.f, 0.f);
+#pragma unroll
+  for (int q = 1; q < KW; ++q) {
+    const int l = lb - q;
+    hist[q] = (q < p.K && l >= 0) ? mk2(ld<T>(xb + phys(l) * p.x.s1 + c), ld<T>(xb + phys(l) * p.x.s1 + c + 1))
+                                  : mk2(0.f, 0.f);
+  }
+  const long long os = rev ? -p.so1 : p.so1;
+  T* op = ob + phys(lb) * p.so1 + c;
+  for (int l0 = lb, k = 0; l0 < le; l0 += kConvST, ++k) {
+    const int stg = k & 1;
+    if (l0 + kConvST < le) issue(stg ^ 1, l0 + kConvST);
+    else asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();  // chunk k visible to all threads
+    const int n = min(kConvST, le - l0);
+#pragma unroll 8
+    for (int j = 0; j < n; ++j) {
+      if constexpr (sizeof(T) == 4) {
+        const float2 v = *reinterpret_cast<const float2*>(&ring[stg][j][c]);
+        hist[0] = mk2(v.x, v.y);
+      } else {
+        const unsigned u = *reinterpret_cast<const unsigned*>(&ring[stg][j][c]);
+        hist[0] = mk2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+      }
+      f2 acc = bias;
+#pragma unroll
+      for (int q = KW - 1; q >= 0; --q) acc = fma2(w[q], hist[q], acc);
+      if (act) acc = mk2(silu_f(acc.x), silu_f(acc.y));
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float2*>(op) = make_float2(acc.x, acc.y);
+      } else {
+        *reinterpret_cast<__nv_bfloat162*>(op) = __floats2bfloat162_rn(acc.x, acc.y);
+      }
+      op += os;
+#pragma unroll
+      for (int q = KW - 1; q >= 1; --q) hist[q] = hist[q - 1];
+    }
+    __syncthreads();  // all reads of stage stg done before it is refilled
+  }
+}
+
 template <typename T>
 static bool conv_vec_ok(const ConvParams& p) {
   constexpr int V = 16 / sizeof(T);
@@ -618,9 +631,16 @@ template <typename T>
 static cudaError_t conv_fwd_t(const ConvParams& p, cudaStream_t st) {
   if constexpr (std::is_same<T, float>::value || std::is_same<T, __nv_bfloat16>::value) {
     if (conv_vec_ok<T>(p) && p.E % kConvTE == 0) {
-      dim3 grid(p.E / kConvTE, (p.L + kConvTT - 1) / kConvTT, p.Bt);
-      if (p.K <= 4) conv_fwd_tile2_kernel<T, 4><<<grid, kConvTE / 2, 0, st>>>(p);
-      else conv_fwd_tile2_kernel<T, kMaxWidth><<<grid, kConvTE / 2, 0, st>>>(p);
+      // rows per CTA: split L so that ~8 CTAs per SM are resident over the grid
+      const long long units = (long long)(p.E / kConvTE) * p.Bt;
+      long long splits = ((long long)LBS_CONV_CTAS_PER_SM * conv_num_sms() + units - 1) / units;
+      const long long max_splits = (p.L + kConvST - 1) / kConvST;
+      if (splits > max_splits) splits = max_splits;
+      if (splits < 1) splits = 1;
+      int rows = (int)((p.L + splits - 1) / splits);
+      dim3 grid(p.E / kConvTE, (unsigned)((p.L + rows - 1) / rows), p.Bt);
+      if (p.K <= 4) conv_fwd_stream_kernel<T, 4><<<grid, 64, 0, st>>>(p, rows);
+      else conv_fwd_stream_kernel<T, kMaxWidth><<<grid, 64, 0, st>>>(p, rows);
       return cudaGetLastError();
     }
   }
