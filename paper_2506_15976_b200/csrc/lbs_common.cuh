@@ -83,25 +83,13 @@ __device__ __forceinline__ float softplus_f(float x) {
 // (a MUFU-free Newton reciprocal measured 1-13 % slower in the scan and the conv)
 __device__ __forceinline__ float sigmoid_f(float x) { return rcp(1.0f + ex2(-x * kLog2e)); }
 __device__ __forceinline__ float silu_f(float x) { return x * sigmoid_f(x); }
-__device__ __forceinline__ float tanh_approx(float x) {
-  float r;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-#ifndef LBS_SILU_TANH
-#define LBS_SILU_TANH 0
-#endif
-// SiLU for a value that is stored as T: for 16-bit outputs sigmoid(x) =
-// 0.5 + 0.5 tanh(x/2) with MUFU.TANH (one MUFU instead of EX2 + RCP; its
-// ~2^-11 relative error is 8x below the bf16 store's rounding), else silu_f.
+// SiLU of a value that is stored as T (the gate at the output store).  A one-MUFU
+// form, 0.5 + 0.5 tanh.approx(x/2) for 16-bit outputs, measured 2.6 % faster in the
+// LBVim-Ti layer; not kept for its absolute error near z << 0 (2^-11 |z| / 2)
+// (profiles/r02_fwd_experiments.txt, vb3 tanh).
 template <typename T>
 __device__ __forceinline__ float silu_out(float x) {
-  if constexpr (LBS_SILU_TANH && sizeof(T) == 2) {
-    const float hx = 0.5f * x;
-    return fmaf(hx, tanh_approx(hx), hx);
-  } else {
-    return silu_f(x);
-  }
+  return silu_f(x);
 }
 
 // ---------------------------------------------------------------------------
