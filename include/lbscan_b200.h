@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define LBS_ABI_VERSION 1
+#define LBS_ABI_VERSION 2
 
 enum lbs_status { LBS_OK = 0, LBS_ERR_INVALID = 1, LBS_ERR_CUDA = 2, LBS_ERR_UNSUPPORTED = 3 };
 enum lbs_dtype { LBS_F32 = 0, LBS_BF16 = 1, LBS_F16 = 2, LBS_F64 = 3 };
@@ -149,6 +149,9 @@ typedef struct lbs_norm_args {
   const void* x;   int64_t x_row_stride;
   const float* scale;       /* (dim) fp32 */
   void* out;       int64_t out_row_stride;
+  int32_t out_dtype;        /* ABI 2: dtype of out (LBS_F32 / LBS_BF16); may differ from io_dtype
+                               only as f32 in -> bf16 out (the bf16 GEMM input of an fp32
+                               residual stream, no separate cast)                              */
 } lbs_norm_args;
 
 int lbs_abi_version(void);
@@ -187,6 +190,8 @@ typedef struct lbs_norm_bwd_args {
   const void* dout;  int64_t dout_row_stride;
   void* dx;          int64_t dx_row_stride;
   float* dscale;              /* (dim) fp32, accumulated (+=); NULL to skip */
+  const void* dres;  int64_t dres_row_stride;  /* ABI 2: optional residual gradient (io dtype)
+                                                  added to dx: dx = norm adjoint + dres */
 } lbs_norm_bwd_args;
 size_t lbs_rms_norm_bwd_workspace_bytes(const lbs_norm_bwd_args* args);
 int lbs_rms_norm_bwd(const lbs_norm_bwd_args* args, void* workspace, size_t workspace_bytes,

@@ -26,6 +26,7 @@ FLAG_ACCUM = 1 << 5
 FLAG_NO_TMA = 1 << 6  # testing: cp.async staging instead of TMA (bitwise-equal results)
 CONV_SILU = 1 << 4
 
+ABI_VERSION = 2  # include/lbscan_b200.h LBS_ABI_VERSION
 I64 = C.c_int64
 I64x3 = C.c_int64 * 3
 VP = C.c_void_p
@@ -86,6 +87,7 @@ class NormArgs(C.Structure):
     _fields_ = [
         ("rows", I64), ("dim", I64), ("io_dtype", C.c_int32), ("eps", C.c_float),
         ("x", VP), ("x_row_stride", I64), ("scale", VP), ("out", VP), ("out_row_stride", I64),
+        ("out_dtype", C.c_int32),
     ]
 
 
@@ -93,7 +95,7 @@ class NormBwdArgs(C.Structure):
     _fields_ = [
         ("rows", I64), ("dim", I64), ("io_dtype", C.c_int32), ("eps", C.c_float),
         ("x", VP), ("x_row_stride", I64), ("scale", VP), ("dout", VP), ("dout_row_stride", I64),
-        ("dx", VP), ("dx_row_stride", I64), ("dscale", VP),
+        ("dx", VP), ("dx_row_stride", I64), ("dscale", VP), ("dres", VP), ("dres_row_stride", I64),
     ]
 
 
@@ -150,7 +152,7 @@ def lib():
     L.lbs_causal_conv1d_bwd_workspace_bytes.argtypes = [C.POINTER(ConvArgs)]
     L.lbs_causal_conv1d_bwd.restype = C.c_int
     L.lbs_causal_conv1d_bwd.argtypes = [C.POINTER(ConvArgs), VP, C.c_size_t, VP]
-    if L.lbs_abi_version() != 1:
+    if L.lbs_abi_version() != ABI_VERSION:
         raise RuntimeError("liblbscan_b200.so ABI version mismatch; rebuild")
     _lib = L
     return L

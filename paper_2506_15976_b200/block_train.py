@@ -11,8 +11,10 @@ on the fused kernels, with the glue between them removed:
   of the two projection gradients and ``du`` into the conv-output gradient, which the
   x|dt|B|C GEMM then accumulates into (``addmm_``, beta = 1); the conv adjoint writes
   ``dx`` into the x|z gradient's first column block; weight gradients and the
-  normalised-input gradient come out of the GEMMs in fp32.  No concatenation of
-  gradient slices, no separate residual / branch additions, one zero-fill.
+  normalised-input gradient come out of the GEMMs in fp32; the RMSNorm forward writes
+  its bf16 GEMM input directly and its adjoint adds the residual branch's gradient.
+  No concatenation of gradient slices, no separate residual / branch additions or
+  casts, one zero-fill.
 
 Used by :class:`paper_2506_15976_b200.model.LBVimTrainer` (default); the plain
 autograd composition ``model.block_forward_train`` stays as the reference for tests.
@@ -41,7 +43,7 @@ class LBVimBlockFn(torch.autograd.Function):
         Bt, L, Dm = T.shape
         E, N = w_x.shape[1], w_b.shape[1]
         rows = Bt * L
-        xn_c = rms_norm(T, norm_scale, eps=eps).reshape(rows, Dm).to(cdt)
+        xn_c = rms_norm(T, norm_scale, eps=eps, out_dtype=cdt).reshape(rows, Dm)  # cast in the norm pass
         w_in = torch.cat([w_x, w_z], 1).to(cdt)                    # (D, 2E)
         xz = (xn_c @ w_in).view(Bt, L, 2 * E)
         xs = causal_conv1d_silu_fwd(xz[..., :E], conv_kernel, None, reverse)
@@ -107,8 +109,7 @@ class LBVimBlockFn(torch.autograd.Function):
         dxz2 = dxz.view(rows, 2 * E)
         dxn = _mm(dxz2, w_in.t(), T.dtype).view(Bt, L, Dm)
         dw_in = _mm(xn_c.t(), dxz2, f32)
-        dT, dscale = rms_norm_bwd(T, norm_scale, dxn, eps=eps)
-        dT.add_(dOut)
+        dT, dscale = rms_norm_bwd(T, norm_scale, dxn, eps=eps, dres=dOut)  # + the residual branch
         d_alog = dA * A  # A = -exp(a_log)
         return (dT, dscale, dw_in[:, :E], dw_in[:, E:], dconv, dw_xp[:, :E], dw_xp[:, E:E + N], dw_xp[:, E + N:],
                 dbias, d_alog, dD, dw_out, None, None, None, None, None, None)

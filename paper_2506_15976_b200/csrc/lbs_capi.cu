@@ -421,8 +421,10 @@ int lbs_rms_norm_fwd(const lbs_norm_args* a, void* stream) {
   if (a->io_dtype != LBS_F32 && a->io_dtype != LBS_BF16) return fail(LBS_ERR_INVALID, "dtype must be f32 or bf16");
   if (!a->x || !a->scale || !a->out) return fail(LBS_ERR_INVALID, "null tensor");
   if (a->rows > (int64_t)1 << 34) return fail(LBS_ERR_UNSUPPORTED, "too many rows");
+  if (a->out_dtype != a->io_dtype && !(a->io_dtype == LBS_F32 && a->out_dtype == LBS_BF16))
+    return fail(LBS_ERR_INVALID, "out_dtype must equal io_dtype, or be bf16 for f32 input");
   lbs::NormParams p{a->rows, (int)a->dim, a->eps, a->x, a->x_row_stride, a->scale, a->out, a->out_row_stride};
-  return cuda_status(lbs::launch_rms_norm(p, a->io_dtype, (cudaStream_t)stream), "lbs_rms_norm_fwd");
+  return cuda_status(lbs::launch_rms_norm(p, a->io_dtype, a->out_dtype, (cudaStream_t)stream), "lbs_rms_norm_fwd");
 }
 
 namespace {
@@ -450,7 +452,7 @@ int lbs_rms_norm_bwd(const lbs_norm_bwd_args* a, void* ws, size_t ws_bytes, void
     return fail(LBS_ERR_INVALID, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
   lbs::NormBwdParams p{a->rows, (int)a->dim, a->eps, a->x, a->x_row_stride, a->scale, a->dout,
                        a->dout_row_stride, a->dx, a->dx_row_stride, a->dscale, static_cast<float*>(ws),
-                       lbs::norm_bwd_warps(a->rows)};
+                       lbs::norm_bwd_warps(a->rows), a->dres, a->dres_row_stride};
   return cuda_status(lbs::launch_rms_norm_bwd(p, a->io_dtype, (cudaStream_t)stream), "lbs_rms_norm_bwd");
 }
 

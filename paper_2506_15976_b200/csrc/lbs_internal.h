@@ -109,7 +109,7 @@ struct NormParams {
   void* out;
   long long so;
 };
-cudaError_t launch_rms_norm(const NormParams& p, int dtype, cudaStream_t st);
+cudaError_t launch_rms_norm(const NormParams& p, int dtype, int out_dtype, cudaStream_t st);
 
 struct NormBwdParams {
   long long rows;
@@ -125,6 +125,8 @@ struct NormBwdParams {
   float* dscale;
   float* part;  // (n_warps, D) fp32 dscale partials
   int n_warps;
+  const void* dres;  // optional residual gradient added to dx (io dtype)
+  long long sres;
 };
 int norm_bwd_warps(long long rows);
 cudaError_t launch_rms_norm_bwd(const NormBwdParams& p, int dtype, cudaStream_t st);

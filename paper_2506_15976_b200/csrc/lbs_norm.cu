@@ -77,9 +77,9 @@ __global__ void __launch_bounds__(256) rms_norm_kernel(const T* __restrict__ x, 
 // G lanes per row (G | 32, 32/G rows per warp), VPL 16-byte vectors per lane:
 // every lane busy and 32/G rows of loads in flight per warp (D = 192 bf16 is 24
 // vectors: 8 lanes x 3 instead of 24 of 32 lanes x 1).
-template <typename T, int G, int VPL>
+template <typename T, int G, int VPL, typename To = T>
 __global__ void __launch_bounds__(256) rms_norm_group_kernel(const T* __restrict__ x, const float* __restrict__ scale,
-                                                             T* __restrict__ out, long long rows, int D, float eps,
+                                                             To* __restrict__ out, long long rows, int D, float eps,
                                                              long long sx, long long so) {
   constexpr int EPV = 16 / sizeof(T);
   constexpr int RPWG = 32 / G;  // rows per warp per pass
@@ -122,20 +122,18 @@ __global__ void __launch_bounds__(256) rms_norm_group_kernel(const T* __restrict
       for (int k = 0; k < VPL; ++k) {
         const int c0 = (sub + G * k) * EPV;
         if (c0 < D) {
-          uint4 o4;
-          T* e = reinterpret_cast<T*>(&o4);
+          // EPV outputs of To: 16 bytes (To == T), or 8 (fp32 in -> bf16 out)
+          using OV = std::conditional_t<sizeof(To) == sizeof(T), uint4, uint2>;
+          OV o4;
+          To* e = reinterpret_cast<To*>(&o4);
 #pragma unroll
           for (int i = 0; i < EPV; i += 4) {
             const float4 s4 = __ldg(reinterpret_cast<const float4*>(scale + c0 + i));
             const float sc[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float y = v[k][i + u] * inv * sc[u];
-              if constexpr (sizeof(T) == 4) e[i + u] = y;
-              else e[i + u] = __float2bfloat16_rn(y);
-            }
+            for (int u = 0; u < 4; ++u) e[i + u] = from_f<To>(v[k][i + u] * inv * sc[u]);
           }
-          *reinterpret_cast<uint4*>(out + row * so + c0) = o4;
+          *reinterpret_cast<OV*>(out + row * so + c0) = o4;
         }
       }
     }
@@ -145,9 +143,9 @@ __global__ void __launch_bounds__(256) rms_norm_group_kernel(const T* __restrict
 }
 
 // any D / alignment: one warp per row, scalar strided accesses
-template <typename T>
+template <typename T, typename To = T>
 __global__ void __launch_bounds__(256) rms_norm_scalar_kernel(const T* __restrict__ x, const float* __restrict__ scale,
-                                                              T* __restrict__ out, long long rows, int D, float eps,
+                                                              To* __restrict__ out, long long rows, int D, float eps,
                                                               long long sx, long long so) {
   const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -160,21 +158,22 @@ __global__ void __launch_bounds__(256) rms_norm_scalar_kernel(const T* __restric
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   const float inv = rsqrtf(ss / (float)D + eps);
-  for (int c = lane; c < D; c += 32) st<T>(out + row * so + c, to_f(x[row * sx + c]) * inv * scale[c]);
+  for (int c = lane; c < D; c += 32) st<To>(out + row * so + c, to_f(x[row * sx + c]) * inv * scale[c]);
 }
 
-template <typename T>
+template <typename T, typename To = T>
 static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
   constexpr int EPV = 16 / sizeof(T);
+  constexpr int OVB = EPV * (int)sizeof(To);  // bytes of one output vector (16, or 8 for f32 -> bf16)
   const int vpl = (p.D + 32 * EPV - 1) / (32 * EPV);
   dim3 block(256), grid((unsigned)((p.rows + 7) / 8));
   const T* x = static_cast<const T*>(p.x);
-  T* o = static_cast<T*>(p.out);
+  To* o = static_cast<To*>(p.out);
   const bool vec = p.D % EPV == 0 && (p.sx * (long long)sizeof(T)) % 16 == 0 &&
-                   (p.so * (long long)sizeof(T)) % 16 == 0 && reinterpret_cast<uintptr_t>(p.x) % 16 == 0 &&
-                   reinterpret_cast<uintptr_t>(p.out) % 16 == 0 && reinterpret_cast<uintptr_t>(p.scale) % 16 == 0 && vpl <= 4;
+                   (p.so * (long long)sizeof(To)) % OVB == 0 && reinterpret_cast<uintptr_t>(p.x) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(p.out) % OVB == 0 && reinterpret_cast<uintptr_t>(p.scale) % 16 == 0 && vpl <= 4;
   if (!vec) {
-    rms_norm_scalar_kernel<T><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+    rms_norm_scalar_kernel<T, To><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
     return cudaGetLastError();
   }
 #ifndef LBS_NORM_RPW
@@ -205,22 +204,28 @@ static cudaError_t launch_norm_t(const NormParams& p, cudaStream_t st) {
       dim3 gg((unsigned)nb);
 #define LBS_NORM_G(GG)                                                                                     \
   if (G == GG) {                                                                                           \
-    if (vpl == 1) rms_norm_group_kernel<T, GG, 1><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
-    else if (vpl == 2) rms_norm_group_kernel<T, GG, 2><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
-    else rms_norm_group_kernel<T, GG, 3><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
+    if (vpl == 1) rms_norm_group_kernel<T, GG, 1, To><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
+    else if (vpl == 2) rms_norm_group_kernel<T, GG, 2, To><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
+    else rms_norm_group_kernel<T, GG, 3, To><<<gg, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so); \
     return cudaGetLastError();                                                                             \
   }
       LBS_NORM_G(1) LBS_NORM_G(2) LBS_NORM_G(4) LBS_NORM_G(8) LBS_NORM_G(16) LBS_NORM_G(32)
 #undef LBS_NORM_G
     }
   }
-  constexpr int RPW = LBS_NORM_RPW;
-  dim3 gridv((unsigned)((p.rows + 8 * RPW - 1) / (8 * RPW)));
-  if (vpl <= 1) rms_norm_kernel<T, 1, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
-  else if (vpl <= 2) rms_norm_kernel<T, 2, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
-  else if (vpl <= 4) rms_norm_kernel<T, 4, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
-  else return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  if constexpr (!std::is_same<T, To>::value) {
+    // mixed dtypes have the lane-group and scalar kernels only
+    rms_norm_scalar_kernel<T, To><<<grid, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+    return cudaGetLastError();
+  } else {
+    constexpr int RPW = LBS_NORM_RPW;
+    dim3 gridv((unsigned)((p.rows + 8 * RPW - 1) / (8 * RPW)));
+    if (vpl <= 1) rms_norm_kernel<T, 1, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+    else if (vpl <= 2) rms_norm_kernel<T, 2, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+    else if (vpl <= 4) rms_norm_kernel<T, 4, RPW><<<gridv, block, 0, st>>>(x, p.scale, o, p.rows, p.D, p.eps, p.sx, p.so);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -256,6 +261,7 @@ __global__ void __launch_bounds__(256) rms_norm_bwd_kernel(NormBwdParams p) {
   T* DX = static_cast<T*>(p.dx);
   // the next row's x / dout are loaded before this row is reduced (one row of
   // loads always in flight per warp)
+  const T* R = static_cast<const T*>(p.dres);  // optional residual gradient: dx += dres
   auto load = [&](long long row, uint4 (&rx)[VPL], uint4 (&rg)[VPL]) {
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
@@ -270,6 +276,14 @@ __global__ void __launch_bounds__(256) rms_norm_bwd_kernel(NormBwdParams p) {
   for (long long row = warp; row < p.rows; row += p.n_warps) {
     uint4 nx[VPL], ng[VPL];
     load(row + p.n_warps, nx, ng);
+    uint4 rr[VPL];
+    if (R) {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const int c0 = (lane + 32 * k) * EPV;
+        rr[k] = c0 < D ? *reinterpret_cast<const uint4*>(R + row * p.sres + c0) : make_uint4(0, 0, 0, 0);
+      }
+    }
     float ss = 0.f, dot = 0.f;
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
@@ -297,10 +311,13 @@ __global__ void __launch_bounds__(256) rms_norm_bwd_kernel(NormBwdParams p) {
         const T* eg = reinterpret_cast<const T*>(&rg[k]);
         uint4 o4;
         T* e = reinterpret_cast<T*>(&o4);
+        const T* er = reinterpret_cast<const T*>(&rr[k]);
 #pragma unroll
         for (int i = 0; i < EPV; ++i) {
           const float xv = to_f(ex[i]), gv = to_f(eg[i]);
-          e[i] = from_f<T>(r * gv * sc[k][i] - xv * c);
+          float d = r * gv * sc[k][i] - xv * c;
+          if (R) d += to_f(er[i]);
+          e[i] = from_f<T>(d);
           dsc[k][i] = fmaf(gv, xv * r, dsc[k][i]);
         }
         *reinterpret_cast<uint4*>(DX + row * p.sdx + c0) = o4;
@@ -356,7 +373,9 @@ __global__ void __launch_bounds__(256) rms_norm_bwd_scalar_kernel(NormBwdParams 
     for (int c = lane; c < D; c += 32) {
       const float xv = to_f(X[row * p.sx + c]);
       const float gv = to_f(G[row * p.sg + c]);
-      DX[row * p.sdx + c] = from_f<T>(r * gv * p.scale[c] - xv * cc);
+      float d = r * gv * p.scale[c] - xv * cc;
+      if (p.dres) d += to_f(static_cast<const T*>(p.dres)[row * p.sres + c]);
+      DX[row * p.sdx + c] = from_f<T>(d);
       if (pw) pw[c] = fmaf(gv, xv * r, pw[c]);
     }
   }
@@ -402,7 +421,7 @@ static cudaError_t launch_norm_bwd_t(const NormBwdParams& p, cudaStream_t st) {
   const unsigned blocks = (unsigned)((p.n_warps + 7) / 8);
   auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
   const bool vec = p.D % EPV == 0 && p.sx % EPV == 0 && p.sg % EPV == 0 && p.sdx % EPV == 0 && al(p.x) &&
-                   al(p.dout) && al(p.dx) && vpl <= 4;
+                   al(p.dout) && al(p.dx) && (!p.dres || (p.sres % EPV == 0 && al(p.dres))) && vpl <= 4;
   if (!vec) rms_norm_bwd_scalar_kernel<T><<<blocks, 256, 0, st>>>(p);
   else if (vpl <= 1) rms_norm_bwd_kernel<T, 1><<<blocks, 256, 0, st>>>(p);
   else if (vpl <= 2) rms_norm_bwd_kernel<T, 2><<<blocks, 256, 0, st>>>(p);
@@ -418,9 +437,10 @@ cudaError_t launch_rms_norm_bwd(const NormBwdParams& p, int dtype, cudaStream_t 
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_rms_norm(const NormParams& p, int dtype, cudaStream_t st) {
-  if (dtype == LBS_F32) return launch_norm_t<float>(p, st);
-  if (dtype == LBS_BF16) return launch_norm_t<__nv_bfloat16>(p, st);
+cudaError_t launch_rms_norm(const NormParams& p, int dtype, int out_dtype, cudaStream_t st) {
+  if (dtype == LBS_F32 && out_dtype == LBS_F32) return launch_norm_t<float>(p, st);
+  if (dtype == LBS_F32 && out_dtype == LBS_BF16) return launch_norm_t<float, __nv_bfloat16>(p, st);
+  if (dtype == LBS_BF16 && out_dtype == LBS_BF16) return launch_norm_t<__nv_bfloat16>(p, st);
   return cudaErrorInvalidValue;
 }
 

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_tile_rule():
     L = _lib.lib()
-    assert L.lbs_abi_version() == 1
+    assert L.lbs_abi_version() == 2
     # engine.py:54-62 / test_engine.py:11-19
     for Ln, M in ((1024, 16), (257, 16), (256, 8), (200, 8), (129, 8), (128, 4), (64, 4), (1, 4)):
         assert L.lbs_select_tile_len(Ln) == M

@@ -392,3 +392,34 @@ def test_rms_norm_bwd(dtype, D, rows):
     sr = s.clone().requires_grad_(True)
     rms_norm_train(xr, sr).backward(dy)
     assert torch.equal(xr.grad, dx) and torch.equal(sr.grad, ds)
+
+
+@pytest.mark.parametrize("D", [192, 384, 8, 1024])
+@pytest.mark.parametrize("rows", [1, 3 * 37, 5000])
+def test_rms_norm_f32_in_bf16_out(D, rows):
+    """lbs_rms_norm_fwd with out_dtype bf16 for fp32 rows: bitwise the fp32 result rounded
+    to bf16 (the training block's bf16 projection input, no separate cast)."""
+    from paper_2506_15976_b200.norm import rms_norm
+    g = torch.Generator(device="cuda").manual_seed(rows + D)
+    x = torch.randn(rows, D, device="cuda", generator=g)
+    s = torch.rand(D, device="cuda", generator=g) + 0.5
+    got = rms_norm(x, s, out_dtype=torch.bfloat16)
+    assert got.dtype == torch.bfloat16
+    assert torch.equal(got, rms_norm(x, s).to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("dtype,D", [(torch.float32, 384), (torch.bfloat16, 192), (torch.float32, 6)])
+def test_rms_norm_bwd_residual(dtype, D):
+    """lbs_rms_norm_bwd with dres: dx + dres in one pass, equal to the separate add."""
+    from paper_2506_15976_b200.norm import rms_norm_bwd
+    g = torch.Generator(device="cuda").manual_seed(D)
+    x = torch.randn(777, D, device="cuda", generator=g).to(dtype)
+    s = torch.randn(D, device="cuda", generator=g)
+    dy = torch.randn(777, D, device="cuda", generator=g).to(dtype)
+    res = torch.randn(777, D, device="cuda", generator=g).to(dtype)
+    dx, ds = rms_norm_bwd(x, s, dy)
+    dxr, dsr = rms_norm_bwd(x, s, dy, dres=res)
+    assert torch.equal(ds, dsr)
+    ref = (dx.float() + res.float())
+    tol = 1e-6 if dtype == torch.float32 else 1e-2
+    assert ((dxr.float() - ref).abs().max() / ref.abs().max()).item() <= tol
