@@ -96,6 +96,9 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 #ifndef LBS_FWD_CL
 #define LBS_FWD_CL 16  // steps per staged chunk (raised to the tile length for long windows)
 #endif
+#ifndef LBS_FWD_ONEBAR
+#define LBS_FWD_ONEBAR 1  // 16-step windows, 16-bit I/O: B/C two chunks ahead, one barrier per chunk
+#endif
 
 template <typename Tio, int CLv = LBS_FWD_CL, int CT = kFwdThreads>
 struct FwdCfg {
@@ -555,7 +558,18 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
   SeqStager<Tio, kVec, CL, CT> stager;
   BcStage<Tbc, NS, CL, kVec && bc_async_ok<Tbc, NS>(), kBcIL, CT> bcs;
   __shared__ __align__(8) uint64_t bars[2];
-  float* bcf2 = reinterpret_cast<float*>(smem_raw + Sm::total);  // second B/C table (TMA)
+  float* bcf2 = reinterpret_cast<float*>(smem_raw + Sm::total);  // second B/C table (TMA; kOneBar)
+  // kOneBar (16-step windows, 16-bit I/O, cp.async): the B/C rows of chunk k+1 are staged
+  // two chunks ahead (3-stage raw ring) and converted into the other half of a
+  // double-buffered table while chunk k computes, so a chunk needs ONE CTA barrier (the
+  // table of chunk k was built before it); the third raw stage follows the second table.
+  // Measured: configs[3] LB scan -2.6 %, bitwise equal; the forward-only scan (+1.5 %) and
+  // 8-step windows (LBVim-Ti, +1 %) keep two barriers (profiles/r02_fwd_experiments.txt)
+  constexpr bool kOneBar =
+      LBS_FWD_ONEBAR && kLB && MT > 8 && sizeof(Tio) == 2 && kVec && bc_async_ok<Tbc, NS>() && !kTma;
+  Tbc* raw3 = reinterpret_cast<Tbc*>(smem_raw + Sm::total + Sm::bc_bytes);
+  auto raw_stage = [&](int s3) -> Tbc* { return s3 < 2 ? bcraw + (size_t)s3 * CL * 2 * NS : raw3; };
+  auto table = [&](int s2) -> float* { return s2 ? bcf2 : bcf; };
   Tbc* rawB = bcraw;                                              // TMA: [2][CL][NS] B rows
   Tbc* rawC = bcraw + 2 * CL * NS;                                //      [2][CL][NS] C rows
   const int narr = has_z ? 3 : 2;
@@ -582,6 +596,17 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
       tma_issue(0, c, clen);
     }
     __syncthreads();
+  } else if constexpr (kOneBar) {
+    stager.init(p, b, e0, has_z);
+    bcs.init(p, b);
+    stager.issue(seq, 0, c, clen);
+    bcs.issue(raw_stage(0), 0, c, clen);
+    const int c1 = c + clen;
+    if (c1 < seg_hi) bcs.issue(raw_stage(1), 0, c1, min(CLm, seg_hi - c1));
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    bcs.publish(table(0), raw_stage(0), 0, clen);  // visible after iteration 0's barrier
   } else {
     stager.init(p, b, e0, has_z);
     bcs.init(p, b);
@@ -611,6 +636,18 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
       bcfk = bt;
       __syncthreads();  // table visible; chunk k-1 done with ring stage stg ^ 1
       if (tid == 0 && clen_n > 0) tma_issue(stg ^ 1, cn, clen_n);
+    } else if constexpr (kOneBar) {
+      cp_async_wait_all();
+      __syncthreads();  // seq rows of chunk k, B/C rows of chunk k+1 landed; table k visible;
+                        // compute of chunk k-1 done (its seq stage and table half are free)
+      bcfk = table(stg);
+      if (clen_n > 0) {
+        bcs.publish(table(stg ^ 1), raw_stage((k + 1) % 3), 0, clen_n);
+        stager.issue(seq, stg ^ 1, cn, clen_n);
+        const int c2 = cn + clen_n;
+        if (c2 < seg_hi) bcs.issue(raw_stage((k + 2) % 3), 0, c2, min(CLm, seg_hi - c2));
+      }
+      cp_async_commit();
     } else {
       cp_async_wait_all();
       __syncthreads();  // chunk k landed (all threads); compute of chunk k-1 done
@@ -844,7 +881,9 @@ inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
   using SmT = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT), CT>;
   // TMA-staged instantiations exist for fp32 I/O only (the launch policy, lbs_capi.cu)
   constexpr bool kTmaOk = LBS_FWD_TMA && kVec && bc_async_ok<Tbc, NS>() && (sizeof(Tio) == 4 || LBS_FWD_TMA_BF16);
-  const size_t smem = SmT::total;  // (+ the second B/C table for the TMA-staged instantiations)
+  // + the second B/C table and the third raw B/C stage for the one-barrier (16-bit, aligned) kernels
+  constexpr bool kOneBarL = LBS_FWD_ONEBAR && MT > 8 && sizeof(Tio) == 2 && kVec && bc_async_ok<Tbc, NS>();
+  const size_t smem = SmT::total + (kOneBarL ? SmT::bc_bytes + (size_t)fwd_chunk(MT) * 2 * NS * sizeof(Tbc) : 0);
   FwdParams pk = p;
   if (!kTmaOk) pk.tma_maps = nullptr;
   dim3 block(CT);
