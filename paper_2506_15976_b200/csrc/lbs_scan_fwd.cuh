@@ -470,7 +470,12 @@ __device__ __forceinline__ void tile_compute(const Tio* su, const Tio* sd, const
 }
 
 // chunk length of the main kernel: LBS_FWD_CL, but at least one whole tile
-constexpr int fwd_chunk(int mt) { return mt > LBS_FWD_CL ? mt : LBS_FWD_CL; }
+#ifndef LBS_FWD_CL16
+#define LBS_FWD_CL16 32  // 16-step windows with 16-bit I/O: steps per staged chunk
+#endif
+constexpr int fwd_chunk(int mt, int io_bytes = 4) {
+  return (mt > 8 && io_bytes == 2) ? LBS_FWD_CL16 : (mt > LBS_FWD_CL ? mt : LBS_FWD_CL);
+}
 
 #ifndef LBS_FWD_MINB
 #define LBS_FWD_MINB 4
@@ -484,7 +489,7 @@ template <typename Tio, typename Tbc, int NS, int MT, bool kLB, bool kVec, bool 
 __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) * (kFwdThreads / CT))
     fwd_kernel(FwdParams p, const __grid_constant__ std::conditional_t<kTma, FwdTmaMaps, NoMaps> tmaps) {
   constexpr int NP = NS / 2;
-  constexpr int CL = fwd_chunk(MT);
+  constexpr int CL = fwd_chunk(MT, sizeof(Tio));
   using Sm = FwdSmem<Tio, Tbc, NS, CL, CT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Tio* seq = reinterpret_cast<Tio*>(smem_raw);
@@ -878,12 +883,12 @@ __global__ void __launch_bounds__(128) segment_prefix_kernel(FwdParams p) {
 
 template <typename Tio, typename Tbc, int NS, int MT, bool kVec, int CT>
 inline cudaError_t launch_fwd_t(const FwdParams& p, cudaStream_t st) {
-  using SmT = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT), CT>;
+  using SmT = FwdSmem<Tio, Tbc, NS, fwd_chunk(MT, sizeof(Tio)), CT>;
   // TMA-staged instantiations exist for fp32 I/O only (the launch policy, lbs_capi.cu)
   constexpr bool kTmaOk = LBS_FWD_TMA && kVec && bc_async_ok<Tbc, NS>() && (sizeof(Tio) == 4 || LBS_FWD_TMA_BF16);
   // + the second B/C table and the third raw B/C stage for the one-barrier (16-bit, aligned) kernels
   constexpr bool kOneBarL = LBS_FWD_ONEBAR && MT > 8 && sizeof(Tio) == 2 && kVec && bc_async_ok<Tbc, NS>();
-  const size_t smem = SmT::total + (kOneBarL ? SmT::bc_bytes + (size_t)fwd_chunk(MT) * 2 * NS * sizeof(Tbc) : 0);
+  const size_t smem = SmT::total + (kOneBarL ? SmT::bc_bytes + (size_t)fwd_chunk(MT, sizeof(Tio)) * 2 * NS * sizeof(Tbc) : 0);
   FwdParams pk = p;
   if (!kTmaOk) pk.tma_maps = nullptr;
   dim3 block(CT);
