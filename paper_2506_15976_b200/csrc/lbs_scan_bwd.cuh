@@ -626,7 +626,9 @@ __global__ void __launch_bounds__(kBwdThreads, LBS_BWD_MINB) bwd_kernel(BwdParam
   const View3D views[4] = {p.u, p.delta, zv, P.dout};
   BwdStager<Tio, kVec, KT> stager;
   stager.init(views, L, rev, b, e0, p.E);
-  BcStage<Tbc, NS, KT, kVec && bc_async_ok<Tbc, NS>(), true> bcs;  // interleaved fp32 table, cp.async when aligned
+  // interleaved fp32 table, cp.async when aligned; the scalar table build (the vectorised
+  // one measured +1.8 % on the configs[2] backward)
+  BcStage<Tbc, NS, KT, kVec && bc_async_ok<Tbc, NS>(), true, kBwdThreads, false> bcs;
   bcs.init(p, b);
   const bool one_tile = m == KT;
   const f2* ckg = reinterpret_cast<const f2*>(p.ckpt) + (long long)b * nck * NP * p.E + ec;

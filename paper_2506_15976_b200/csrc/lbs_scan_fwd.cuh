@@ -235,11 +235,14 @@ struct BcPrefetch {
 template <typename Tbc, int NS>
 __host__ __device__ constexpr bool bc_async_ok() { return (NS * sizeof(Tbc)) % 16 == 0; }
 
+#ifndef LBS_BC_PUBLISH_VEC
+#define LBS_BC_PUBLISH_VEC 1
+#endif
 // B/C staging for one chunk.  kAsync (N == NS, rows of 16-byte pieces): the
 // raw rows are copied by cp.async into a 2-stage shared-memory ring together
 // with u/delta/z — a global load the compiler cannot sink to its use — and
 // converted to the fp32 broadcast table at publish.  Otherwise: BcPrefetch.
-template <typename Tbc, int NS, int CL, bool kAsync, bool kIL = false, int CT = kFwdThreads>
+template <typename Tbc, int NS, int CL, bool kAsync, bool kIL = false, int CT = kFwdThreads, bool kVecPub = true>
 struct BcStage {
   static constexpr int EPB = 16 / sizeof(Tbc);   // elements per 16-byte piece
   static constexpr int PB = NS / EPB;            // pieces per B (or C) row
@@ -274,7 +277,37 @@ struct BcStage {
     }
   }
   __device__ __forceinline__ void publish(float* bcf, const Tbc* raw, int stg, int clen) {
-    if constexpr (kAsync) {
+    if constexpr (kAsync && kIL && kVecPub && LBS_BC_PUBLISH_VEC) {
+      // one 16-byte piece per (step, B|C, piece): a 16-byte shared load, the state pairs
+      // (n, n+1) converted with bit moves and written as the table's 8-byte pair slots
+      // (the scalar form was a load -> convert -> store chain per value with a branch,
+      // 13 % of the stall samples at configs[3])
+      constexpr int UNITS = CL * 2 * PB;
+#pragma unroll
+      for (int u0 = 0; u0 < UNITS; u0 += CT) {
+        const int u = u0 + threadIdx.x;
+        if (UNITS % CT == 0 || u < UNITS) {
+          const int t = u / (2 * PB), rr = u % (2 * PB);
+          const int w = rr / PB, pc = rr % PB;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (t < clen)
+            v = *reinterpret_cast<const uint4*>(raw + ((size_t)(stg * CL + t) * 2 * NS + w * NS + pc * EPB));
+          float* row = bcf + t * 2 * NS + w * 2;  // pair q at row[q * 4]
+          const unsigned wd[4] = {v.x, v.y, v.z, v.w};
+          if constexpr (sizeof(Tbc) == 2) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)  // word j: states pc*8 + 2j (low half), + 2j + 1 (high half)
+              *reinterpret_cast<float2*>(row + (pc * 4 + j) * 4) =
+                  make_float2(__uint_as_float(wd[j] << 16), __uint_as_float(wd[j] & 0xffff0000u));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)  // states pc*4 + 2j, + 2j + 1
+              *reinterpret_cast<float2*>(row + (pc * 2 + j) * 4) =
+                  make_float2(__uint_as_float(wd[2 * j]), __uint_as_float(wd[2 * j + 1]));
+          }
+        }
+      }
+    } else if constexpr (kAsync) {
 #pragma unroll
       for (int i0 = 0; i0 < CL * 2 * NS; i0 += CT) {
         const int i = i0 + threadIdx.x;
