@@ -663,13 +663,31 @@ __global__ void __launch_bounds__(CT, (MT <= 8 ? LBS_FWD_MINB : LBS_FWD_MINB16) 
       mbar_wait(&bars[stg], (k >> 1) & 1);
       float* bt = stg ? bcf2 : bcf;
       if (rev) { rs = -CT; rb = clen - 1; }
-      // B/C rows -> fp32 broadcast table in logical order
-      for (int i = tid; i < CL * 2 * NS; i += CT) {
-        const int t = i / (2 * NS), kk = i % (2 * NS);
-        const int w = kk / NS, n = kk % NS;
-        const int row = rev ? clen - 1 - t : t;
-        const Tbc* src = (w ? rawC : rawB) + ((size_t)stg * CL + row) * NS + n;
-        bt[bc_index<NS, kBcIL>(t, w, n)] = t < clen ? to_f(*src) : 0.f;
+      // B/C rows -> fp32 broadcast table in logical order: one 16-byte piece per
+      // (step, B|C, piece), pairs written as the table's 8-byte slots (as BcStage::publish)
+      {
+        constexpr int EPB = 16 / sizeof(Tbc), PB = NS / EPB;
+        for (int u = tid; u < CL * 2 * PB; u += CT) {
+          const int t = u / (2 * PB), rr = u % (2 * PB);
+          const int w = rr / PB, pc = rr % PB;
+          const int row = rev ? clen - 1 - t : t;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (t < clen)
+            v = *reinterpret_cast<const uint4*>((w ? rawC : rawB) + ((size_t)stg * CL + row) * NS + pc * EPB);
+          float* trow = bt + t * 2 * NS + w * 2;
+          const unsigned wd[4] = {v.x, v.y, v.z, v.w};
+          if constexpr (sizeof(Tbc) == 2) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<float2*>(trow + (pc * 4 + j) * 4) =
+                  make_float2(__uint_as_float(wd[j] << 16), __uint_as_float(wd[j] & 0xffff0000u));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              *reinterpret_cast<float2*>(trow + (pc * 2 + j) * 4) =
+                  make_float2(__uint_as_float(wd[2 * j]), __uint_as_float(wd[2 * j + 1]));
+          }
+        }
       }
       bcfk = bt;
       __syncthreads();  // table visible; chunk k-1 done with ring stage stg ^ 1
